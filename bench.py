@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: ToGraph -> PageRank x20 -> triangle count.
+
+One "step" = one pass of the path over one R-MAT table (BASELINE.json
+configs[1] C2 by default: scale 22, 69M int64 rows, seed 2, permuted ids;
+triangles on its symmetrised version = configs[2] C3):
+    table_to_graph  ->  pagerank(d=0.85, 20 iterations, fp64)  ->  triangle_count
+`value` = input rows per second through the whole step (table already in
+HBM); `e2e` = the same through the public Python API with host (pinned)
+columns, host->device copy and result readback inside the timed region;
+`phases` break the step into the three rows of the metric, each in its own
+unit (build rows/s, PageRank edge-iterations/s, triangles undirected edges/s);
+`roofline` is the dominant kernel's algorithmic bytes / measured time vs the
+measured HBM copy peak (MEASURED_PEAKS.json).
+
+`--impl reference` times the reference's own CPU algorithm (the numpy
+restatement in oracle/, the reference being pure Python that is not shipped
+to the GPU box) on a bounded prefix sample of the same table.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+import numpy as np  # noqa: E402
+
+METRIC = "edges/s: table->CSR build, PageRank iteration, triangle count (+% HBM roofline)"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", choices=["c1", "c2", "c4"], default="c2")
+    p.add_argument("--iterations", type=int, default=20)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-rows", type=int, default=1_000_000)
+    return p.parse_args()
+
+
+def peaks():
+    path = REPO / "MEASURED_PEAKS.json"
+    if path.exists():
+        d = json.loads(path.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return PEAKS_FALLBACK
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def spec_for(name):
+    from paper_1503_07881_b200.synth import CONFIGS
+
+    return CONFIGS[name]
+
+
+# ------------------------------------------------------------------ reference
+
+def run_cpu_sample(spec, rows, iterations):
+    """The reference algorithm (oracle port, all host cores) on rows [0, rows)."""
+    from oracle import reference_port as ref
+    from paper_1503_07881_b200.synth import rmat_edges
+
+    src, dst = rmat_edges(spec.scale, rows, spec.a, spec.b, spec.c, spec.seed, spec.permute)
+    t0 = time.perf_counter()
+    g = ref.build_csr(src, dst)
+    t1 = time.perf_counter()
+    ref.pagerank_csr(g, 0.85, iterations)
+    t2 = time.perf_counter()
+    tc = ref.triangle_count_csr(g)
+    t3 = time.perf_counter()
+    return {"rows": rows, "n": g.n, "e": g.e, "tc": tc, "build_s": t1 - t0, "pr_s": t2 - t1,
+            "tc_s": t3 - t2, "total_s": t3 - t0}
+
+
+def cpu_info():
+    model = platform.processor() or ""
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cores": os.cpu_count() or 1, "model": model, "numpy": np.__version__}
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    spec = spec_for(args.config)
+    rows = min(args.cpu_sample_rows, spec.rows)
+    for _ in range(args.warmup):
+        run_cpu_sample(spec, rows, args.iterations)
+    times = []
+    last = None
+    for _ in range(args.steps):
+        last = run_cpu_sample(spec, rows, args.iterations)
+        times.append(last["total_s"])
+    mean = sum(times) / len(times)
+    value = rows / mean
+    info = cpu_info()
+    sample = (f"rows [0,{rows}) of {args.config} (R-MAT s{spec.scale}, seed {spec.seed}, "
+              f"permuted={spec.permute}): build + PageRank x{args.iterations} + triangles; "
+              f"N={last['n']} E={last['e']}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} sample", "rows": rows,
+                   "pagerank_iterations": args.iterations},
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": info["cores"],
+                         "kind": "port", "sample": sample, "cpu": info["model"],
+                         "phases_s": {k: last[k] for k in ("build_s", "pr_s", "tc_s")}},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------- ours
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.dev), "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return None
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def ours_arm(args):
+    import torch
+
+    rank, world, local = dist_env()
+    os.environ["GT_DEVICE"] = str(local)
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1503_07881_b200 as gt
+    from paper_1503_07881_b200 import _native
+    from paper_1503_07881_b200.synth import rmat_device
+
+    spec = spec_for(args.config)
+    dev = torch.device("cuda", local)
+    src, dst = rmat_device(spec, device=f"cuda:{local}")
+    table = gt.edge_table(src, dst)
+    edge_spec = gt.EdgeSpec("src", "dst")
+    stream = torch.cuda.ExternalStream(_native.stream_handle(), device=dev)
+    iters = args.iterations
+    state = {}
+
+    def step():
+        g = gt.table_to_graph(table, edge_spec)
+        out = state.get("scores")
+        if out is None or out.shape[0] != g.node_count:
+            out = state["scores"] = torch.empty(g.node_count, dtype=torch.float64, device=dev)
+        gt.pagerank_device(g, 0.85, iters, out.data_ptr())
+        tc = gt.triangle_count(g)
+        state.update(n=g.node_count, e=g.edge_count, tc=tc)
+        del g
+
+    for _ in range(args.warmup):
+        step()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: K steps, CUDA events on the library stream ----------
+    _native.profile_enable(True)
+    _native.profile_reset()
+    launches0 = _native.launch_count()
+    with ClockSampler(local) as clocks:
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        ev1.synchronize()
+        barrier()
+    launches = _native.launch_count() - launches0
+    elapsed_ms = ev0.elapsed_time(ev1)
+    phases = _native.profile_read()
+    _native.profile_enable(False)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+
+    rows = spec.rows
+    ms_per_step = elapsed_ms / args.steps
+    value = rows * world / (ms_per_step / 1e3)
+    n, e, tc = state["n"], state["e"], state["tc"]
+
+    pk = peaks()
+
+    def group(prefixes):
+        ms = sum(v[0] for k, v in phases.items() if k.startswith(prefixes)) / args.steps
+        by = sum(v[2] for k, v in phases.items() if k.startswith(prefixes)) / args.steps
+        return ms, by
+
+    b_ms, b_bytes = group(("build.", "sort.digit"))
+    p_ms, p_bytes = group(("pr.",))
+    t_ms, t_bytes = group(("tc.",))
+    phase_line = {
+        "build": {"ms": b_ms, "value": rows / (b_ms / 1e3) if b_ms else None, "unit": "rows/s",
+                  "achieved_gbs": b_bytes / (b_ms / 1e3) / 1e9 if b_ms else None},
+        "pagerank": {"ms": p_ms, "value": e * iters / (p_ms / 1e3) if p_ms else None,
+                     "unit": "edge-iterations/s",
+                     "achieved_gbs": p_bytes / (p_ms / 1e3) / 1e9 if p_ms else None},
+        "triangles": {"ms": t_ms, "unit": "undirected edges/s (directed E_d/s in e_d_value)",
+                      "e_d_value": e / (t_ms / 1e3) if t_ms else None,
+                      "triangles": tc},
+    }
+    for k in ("build", "pagerank"):
+        if phase_line[k]["achieved_gbs"]:
+            phase_line[k]["hbm_frac"] = phase_line[k]["achieved_gbs"] / pk["hbm_gbs"]
+
+    kernels = {}
+    for name, (ms, cnt, by) in phases.items():
+        kernels[name] = {"ms_per_step": ms / args.steps, "launches_per_step": cnt / args.steps,
+                         "gbs": (by / (ms / 1e3) / 1e9) if ms > 0 and by > 0 else None}
+    dom_name, (dom_ms, dom_cnt, dom_bytes) = max(phases.items(), key=lambda kv: kv[1][0])
+    dom_gbs = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+    roofline = {"bound": "hbm", "kernel": dom_name,
+                "achieved": dom_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": dom_gbs / pk["hbm_gbs"], "traffic": None,
+                "bytes_per_launch": dom_bytes / max(dom_cnt, 1),
+                "ms_per_launch": dom_ms / max(dom_cnt, 1), "peak_source": pk["source"],
+                "share_of_step": dom_ms / elapsed_ms}
+
+    # ---- end to end through the public API with host buffers ---------------
+    e2e = None
+    if not args.no_e2e:
+        h_src = torch.empty(rows, dtype=torch.int64, pin_memory=True)
+        h_dst = torch.empty(rows, dtype=torch.int64, pin_memory=True)
+        h_src.copy_(src)
+        h_dst.copy_(dst)
+        host_table = gt.edge_table(h_src.numpy(), h_dst.numpy())
+        del table, src, dst
+        state.clear()
+        torch.cuda.empty_cache()
+
+        def e2e_step():
+            g = gt.table_to_graph(host_table, edge_spec)
+            pr = gt.pagerank(g, 0.85, iters)
+            tc_ = gt.triangle_count(g)
+            return pr, tc_
+
+        for _ in range(max(1, min(args.warmup, 2))):
+            e2e_step()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pr, tc2 = e2e_step()
+        e1.record(stream)
+        e1.synchronize()
+        wall = time.perf_counter() - t0
+        barrier()
+        e2e_ms = max(e0.elapsed_time(e1), wall * 1e3) / args.steps
+        if world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        assert tc2 == tc, "e2e triangle count differs from the device-resident run"
+        e2e = {"value": rows * world / (e2e_ms / 1e3), "unit": "rows/s",
+               "ms_per_step": e2e_ms, "h2d_bytes_per_step": 16 * rows,
+               "d2h_bytes_per_step": 16 * n + 8 + 8,
+               "api": "table_to_graph(host ColumnTable) -> pagerank -> triangle_count"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = run_cpu_sample(spec, min(args.cpu_sample_rows, rows), iters)
+        info = cpu_info()
+        cpu = {"value": r["rows"] / r["total_s"], "unit": "rows/s", "cores": info["cores"],
+               "kind": "port",
+               "sample": (f"rows [0,{r['rows']}) of {args.config}: build + PageRank x{iters} + "
+                          f"triangles via oracle/reference_port.py (numpy, workers=all cores), "
+                          f"N={r['n']} E={r['e']}; {r['total_s']:.2f}s"),
+               "cpu": info["model"],
+               "phases_s": {k: r[k] for k in ("build_s", "pr_s", "tc_s")}}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int64+f64", "data": "synthetic (R-MAT generated on device, seeded)",
+        "config": {"workload": f"{args.config}: R-MAT s{spec.scale} {rows} rows seed {spec.seed}"
+                               f" permuted={spec.permute}; ToGraph + PageRank x{iters} fp64 + "
+                               "triangles (C3)",
+                   "rows": rows, "nodes": n, "edges": e, "triangles": tc,
+                   "pagerank_iterations": iters,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (16*rows bytes >> 126 MB)"},
+        "phases": phase_line, "kernels": kernels, "roofline": roofline,
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return ours_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,151 @@
+/*
+ * gtb200.h — C ABI of the B200-native graphtables hot path.
+ *
+ * One shared library (libgtb200.so, sm_100a) replaces the three numpy
+ * routines that dominate Ringo-style analytics in the reference package
+ * (`/root/reference/pkg/src/graphtables`):
+ *
+ *   gt_build_csr   replaces convert.table_to_graph          (convert.py:128-175)
+ *                  together with _dense_ids / _pack / _sorted_unique_pairs /
+ *                  parallel_sort / _fill_pool                (convert.py:45-125,
+ *                                                             parallel.py:52-93)
+ *   gt_pagerank    replaces algorithms.pagerank             (algorithms.py:36-87)
+ *   gt_triangles   replaces algorithms.triangle_count       (algorithms.py:90-119)
+ *   gt_graph_export materialises the reference's in/out pools + offsets
+ *                  (convert.py:154-174) in host memory, ids ascending
+ *                  (graphs.py:80-82: Graph.node_ids()).
+ *
+ * Conventions
+ *  - Every call is synchronous with respect to the caller: it enqueues work on
+ *    the library stream (gt_stream()) and synchronises before returning,
+ *    unless the name ends in `_async`.
+ *  - Return value: GT_OK (0) or one of the GT_E* codes below; the message of
+ *    the last failure on the calling thread is gt_last_error().
+ *  - Pointers named `d_*` are device pointers (HBM), `h_*` host pointers.
+ *    Pointers that may be either carry an explicit `*_is_device` flag.
+ *  - A gt_graph owns all of its device buffers; gt_graph_free releases them.
+ *    Input columns are borrowed and never written (convert.py:138-139).
+ *  - Dense node index = rank of the id among the distinct ids of src ∪ dst in
+ *    ascending signed order (convert.py:51-52); adjacency is stored as int32
+ *    dense indices, offsets as int64 (convert.py:156-157).
+ */
+#ifndef GTB200_H
+#define GTB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (mapped to the reference's exception types by the host shim) */
+#define GT_OK        0
+#define GT_EINVAL    1   /* ValueError / TypeMismatchError                     */
+#define GT_ENOMEM    2   /* MemoryError (device allocation failed)             */
+#define GT_ECUDA     3   /* RuntimeError (CUDA launch / runtime failure)       */
+#define GT_ENCCL     4   /* RuntimeError (collective failure)                  */
+#define GT_ECAPACITY 5   /* CapacityError: N >= 2^31 distinct ids              */
+#define GT_ENODEV    6   /* RuntimeError: no CUDA device / wrong architecture  */
+
+#if defined(__GNUC__)
+#define GT_API __attribute__((visibility("default")))
+#else
+#define GT_API
+#endif
+
+typedef struct gt_graph gt_graph;
+
+/* ---- context ------------------------------------------------------------ */
+
+/* Select the CUDA device for this process and create the library stream.
+ * Idempotent for the same device. Fails with GT_ENODEV when no sm_100 device
+ * is visible. */
+GT_API int gt_init(int device);
+
+/* Library version string and the cudaStream_t (as void*) every kernel runs on. */
+GT_API const char* gt_version(void);
+GT_API void* gt_stream(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+GT_API const char* gt_last_error(void);
+
+/* Release cached scratch memory (radix-sort buffers, look-back state). */
+GT_API int gt_release_workspace(void);
+
+/* ---- table -> CSR  (convert.table_to_graph, convert.py:128-175) ---------- */
+
+/* Build the directed simple graph of the edge table (src[i], dst[i]), i<rows:
+ * node set = distinct ids of src ∪ dst, edge set = distinct (src,dst) pairs,
+ * out-CSR sorted by (src,dst), in-CSR sorted by (dst,src). rows == 0 yields an
+ * empty graph. `cols_are_device` = 1 if src/dst are device pointers, 0 for
+ * host pointers (copied to HBM inside the call). */
+GT_API int gt_build_csr(const int64_t* src, const int64_t* dst, int64_t rows,
+                 int cols_are_device, gt_graph** out);
+
+/* Same, with additional node ids that become nodes even without edges (a
+ * host Graph's isolated nodes, graphs.py:92-96 add_node): node set = distinct
+ * ids of src ∪ dst ∪ nodes. Used to move any Graph to the device. */
+GT_API int gt_build_csr_nodes(const int64_t* src, const int64_t* dst, int64_t rows,
+                              const int64_t* nodes, int64_t n_nodes, int cols_are_device,
+                              gt_graph** out);
+
+/* Node and distinct-edge counts (Graph.node_count / Graph.edge_count,
+ * graphs.py:62-68). */
+GT_API int gt_graph_sizes(const gt_graph* g, int64_t* n_nodes, int64_t* n_edges);
+
+/* Copy the CSR to host memory in the reference's layout: ids[N] ascending,
+ * out_off[N+1], out_adj[E] (original ids, per-node ascending), in_off[N+1],
+ * in_adj[E]. Any pointer may be NULL to skip that array. */
+GT_API int gt_graph_export(const gt_graph* g, int64_t* h_ids, int64_t* h_out_off,
+                    int64_t* h_out_adj, int64_t* h_in_off, int64_t* h_in_adj);
+
+/* Device views of the CSR (dense int32 adjacency), owned by the graph. */
+GT_API int gt_graph_device_views(const gt_graph* g, const int64_t** d_ids,
+                          const int64_t** d_out_off, const int32_t** d_out_adj,
+                          const int64_t** d_in_off, const int32_t** d_in_adj);
+
+GT_API void gt_graph_free(gt_graph* g);
+
+/* ---- PageRank (algorithms.pagerank, algorithms.py:36-87) --------------- */
+
+/* Damped power iteration, fp64, start 1/N, dangling mass redistributed
+ * uniformly; scores[i] belongs to the i-th smallest node id.
+ * `scores_is_device` selects a device or host output buffer of N doubles.
+ * Errors: GT_EINVAL for damping ∉ (0,1), iterations < 1, empty graph
+ * (algorithms.py:45-50). */
+GT_API int gt_pagerank(const gt_graph* g, double damping, int iterations,
+                double* scores, int scores_is_device);
+
+/* ---- triangle count (algorithms.triangle_count, algorithms.py:90-119) -- */
+
+/* Number of unordered mutually adjacent triples of the symmetrised graph,
+ * self-loops ignored; 0 for an empty graph (algorithms.py:100-101). */
+GT_API int gt_triangles(const gt_graph* g, int64_t* count);
+
+/* ---- synthetic inputs (bench / tests; no reference counterpart) --------- */
+
+/* R-MAT edge table generated on the device, bit-identical to the numpy
+ * generator paper_1503_07881_b200.synth.rmat_edges: row e, level l uses
+ * splitmix64(key(seed) + e*scale + l); quadrant thresholds a, a+b, a+b+c on
+ * 53-bit uniforms; optional keyed Feistel permutation of [0, 2^scale). */
+GT_API int gt_rmat_generate(int scale, int64_t rows, double a, double b, double c,
+                     uint64_t seed, int permute, int64_t* d_src, int64_t* d_dst);
+
+/* ---- instrumentation ---------------------------------------------------- */
+
+/* Number of kernels this library has launched since load. */
+GT_API int64_t gt_launch_count(void);
+
+/* Per-phase device time accounting (CUDA events on gt_stream()).
+ * gt_profile_enable(1) starts recording; gt_profile_read fills up to `cap`
+ * entries of (name, total_ms, launches, algorithmic_bytes) and returns the
+ * number of phases; gt_profile_reset clears the totals. */
+GT_API int gt_profile_enable(int on);
+GT_API int gt_profile_reset(void);
+GT_API int gt_profile_read(int cap, const char** names, double* total_ms,
+                    int64_t* launches, double* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GTB200_H */

@@ -1,0 +1,222 @@
+"""ctypes binding of libgtb200.so (declared in include/gtb200.h).
+
+The library is the only compute path: if it is missing or cannot initialise
+a B200, every call raises :class:`NativeError` — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .errors import CapacityError, NativeError
+
+LIB_PATH = Path(__file__).resolve().parent / "libgtb200.so"
+
+GT_OK, GT_EINVAL, GT_ENOMEM, GT_ECUDA, GT_ENCCL, GT_ECAPACITY, GT_ENODEV = range(7)
+
+# Every symbol include/gtb200.h declares, with its ctypes signature.
+_I64P = ctypes.POINTER(ctypes.c_int64)
+_VP = ctypes.c_void_p
+SIGNATURES = {
+    "gt_init": (ctypes.c_int, [ctypes.c_int]),
+    "gt_version": (ctypes.c_char_p, []),
+    "gt_stream": (_VP, []),
+    "gt_last_error": (ctypes.c_char_p, []),
+    "gt_release_workspace": (ctypes.c_int, []),
+    "gt_build_csr": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_int,
+                                    ctypes.POINTER(_VP)]),
+    "gt_build_csr_nodes": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, _VP, ctypes.c_int64,
+                                          ctypes.c_int, ctypes.POINTER(_VP)]),
+    "gt_graph_sizes": (ctypes.c_int, [_VP, _I64P, _I64P]),
+    "gt_graph_export": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
+    "gt_graph_device_views": (ctypes.c_int, [_VP, ctypes.POINTER(_VP), ctypes.POINTER(_VP),
+                                             ctypes.POINTER(_VP), ctypes.POINTER(_VP),
+                                             ctypes.POINTER(_VP)]),
+    "gt_graph_free": (None, [_VP]),
+    "gt_pagerank": (ctypes.c_int, [_VP, ctypes.c_double, ctypes.c_int, _VP, ctypes.c_int]),
+    "gt_triangles": (ctypes.c_int, [_VP, _I64P]),
+    "gt_rmat_generate": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_double,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
+                                        ctypes.c_int, _VP, _VP]),
+    "gt_launch_count": (ctypes.c_int64, []),
+    "gt_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+    "gt_profile_reset": (ctypes.c_int, []),
+    "gt_profile_read": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_char_p),
+                                       ctypes.POINTER(ctypes.c_double), _I64P,
+                                       ctypes.POINTER(ctypes.c_double)]),
+}
+
+_lib = None
+_lock = threading.Lock()
+_initialised = False
+
+
+def load():
+    """dlopen libgtb200.so and declare every entry point (no GPU needed)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise NativeError(
+                    f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; "
+                    "g.build()'` (the CUDA library is the only compute path)")
+            lib = ctypes.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def _raise(rc: int, what: str):
+    msg = load().gt_last_error().decode(errors="replace")
+    text = f"{what}: {msg}"
+    if rc == GT_EINVAL:
+        raise ValueError(text)
+    if rc == GT_ECAPACITY:
+        raise CapacityError(text)
+    if rc == GT_ENOMEM:
+        raise MemoryError(text)
+    raise NativeError(text)
+
+
+def check(rc: int, what: str):
+    if rc != GT_OK:
+        _raise(rc, what)
+
+
+def device_ordinal() -> int:
+    for var in ("GT_DEVICE", "LOCAL_RANK"):
+        if os.environ.get(var):
+            return int(os.environ[var])
+    return 0
+
+
+def ensure_init():
+    global _initialised
+    lib = load()
+    if not _initialised:
+        check(lib.gt_init(device_ordinal()), "gt_init")
+        _initialised = True
+    return lib
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data if a.size else 0
+
+
+def build_csr(src, dst, rows: int, on_device: bool, nodes=None) -> int:
+    """-> opaque gt_graph* (int). src/dst: device pointers or numpy int64."""
+    lib = ensure_init()
+    out = ctypes.c_void_p()
+    if on_device:
+        s, d = int(src), int(dst)
+        keep = ()
+    else:
+        src = np.ascontiguousarray(src, dtype=np.int64)
+        dst = np.ascontiguousarray(dst, dtype=np.int64)
+        s, d, keep = _ptr(src), _ptr(dst), (src, dst)
+    if nodes is None:
+        rc = lib.gt_build_csr(s, d, int(rows), int(on_device), ctypes.byref(out))
+    else:
+        if on_device:
+            nptr, nn = int(nodes[0]), int(nodes[1])
+        else:
+            nodes = np.ascontiguousarray(nodes, dtype=np.int64)
+            nptr, nn = _ptr(nodes), int(nodes.shape[0])
+        rc = lib.gt_build_csr_nodes(s, d, int(rows), nptr, nn, int(on_device),
+                                    ctypes.byref(out))
+    del keep
+    check(rc, "gt_build_csr")
+    return int(out.value)
+
+
+def graph_sizes(handle: int):
+    n, e = ctypes.c_int64(), ctypes.c_int64()
+    check(load().gt_graph_sizes(handle, ctypes.byref(n), ctypes.byref(e)), "gt_graph_sizes")
+    return int(n.value), int(e.value)
+
+
+def graph_export(handle: int, n: int, e: int):
+    ids = np.empty(n, dtype=np.int64)
+    out_off = np.empty(n + 1, dtype=np.int64)
+    out_adj = np.empty(e, dtype=np.int64)
+    in_off = np.empty(n + 1, dtype=np.int64)
+    in_adj = np.empty(e, dtype=np.int64)
+    check(load().gt_graph_export(handle, _ptr(ids), _ptr(out_off), _ptr(out_adj), _ptr(in_off),
+                                 _ptr(in_adj)), "gt_graph_export")
+    return ids, out_off, out_adj, in_off, in_adj
+
+
+def graph_device_views(handle: int):
+    ptrs = [ctypes.c_void_p() for _ in range(5)]
+    check(load().gt_graph_device_views(handle, *[ctypes.byref(p) for p in ptrs]),
+          "gt_graph_device_views")
+    return [int(p.value or 0) for p in ptrs]
+
+
+def graph_free(handle: int):
+    if handle and _lib is not None:
+        _lib.gt_graph_free(handle)
+
+
+def pagerank(handle: int, n: int, damping: float, iterations: int, out_ptr: int | None = None):
+    lib = ensure_init()
+    if out_ptr is not None:
+        check(lib.gt_pagerank(handle, float(damping), int(iterations), int(out_ptr), 1),
+              "gt_pagerank")
+        return None
+    scores = np.empty(n, dtype=np.float64)
+    check(lib.gt_pagerank(handle, float(damping), int(iterations), _ptr(scores), 0),
+          "gt_pagerank")
+    return scores
+
+
+def triangles(handle: int) -> int:
+    lib = ensure_init()
+    c = ctypes.c_int64()
+    check(lib.gt_triangles(handle, ctypes.byref(c)), "gt_triangles")
+    return int(c.value)
+
+
+def rmat_generate(scale, rows, a, b, c, seed, permute, src_ptr, dst_ptr):
+    lib = ensure_init()
+    check(lib.gt_rmat_generate(int(scale), int(rows), float(a), float(b), float(c),
+                               int(seed) & ((1 << 64) - 1), int(bool(permute)), int(src_ptr),
+                               int(dst_ptr)), "gt_rmat_generate")
+
+
+def stream_handle() -> int:
+    return int(ensure_init().gt_stream() or 0)
+
+
+def launch_count() -> int:
+    return int(load().gt_launch_count())
+
+
+def profile_enable(on: bool = True):
+    ensure_init().gt_profile_enable(int(on))
+
+
+def profile_reset():
+    check(load().gt_profile_reset(), "gt_profile_reset")
+
+
+def profile_read():
+    """-> {phase: (total_ms, launches, algorithmic_bytes)}"""
+    lib = load()
+    cap = 64
+    names = (ctypes.c_char_p * cap)()
+    ms = (ctypes.c_double * cap)()
+    launches = (ctypes.c_int64 * cap)()
+    nbytes = (ctypes.c_double * cap)()
+    k = lib.gt_profile_read(cap, names, ms, launches, nbytes)
+    if k < 0:
+        _raise(-k, "gt_profile_read")
+    return {names[i].decode(): (ms[i], int(launches[i]), nbytes[i]) for i in range(min(k, cap))}

@@ -1,0 +1,115 @@
+"""PageRank and triangle counting on the device CSR (libgtb200).
+
+Drop-ins for ``graphtables.algorithms.pagerank`` (algorithms.py:36-87) and
+``triangle_count`` (algorithms.py:90-119): same signatures, validation and
+results (PageRank fp64 within 1e-9 L1 of the reference — GPU summation order
+differs, but is fixed, so runs are bitwise reproducible; triangle counts
+exact). Any graph exposing ``node_ids()``/``record()`` is accepted; host
+graphs are uploaded first (isolated nodes included).
+"""
+
+from __future__ import annotations
+
+from collections.abc import Mapping
+
+import numpy as np
+
+from . import _native
+from .convert import resolve_workers
+from .graph import DeviceGraph, upload
+
+
+class RankMap(Mapping):
+    """Read-only ``{node id: score}`` view over two arrays (ids ascending).
+
+    Returned instead of building a Python dict of N entries
+    (algorithms.py:87): lookups are a binary search, iteration yields ids in
+    ascending order, ``dict(r)`` / ``r.items()`` / ``sum(r.values())`` work.
+    """
+
+    __slots__ = ("ids", "scores")
+
+    def __init__(self, ids: np.ndarray, scores: np.ndarray):
+        self.ids = ids
+        self.scores = scores
+
+    def __getitem__(self, node):
+        try:
+            pos = int(np.searchsorted(self.ids, node))
+        except (TypeError, OverflowError):
+            raise KeyError(node) from None
+        if pos >= self.ids.shape[0] or self.ids[pos] != node:
+            raise KeyError(node)
+        return float(self.scores[pos])
+
+    def __len__(self):
+        return int(self.ids.shape[0])
+
+    def __iter__(self):
+        return iter(self.ids.tolist())
+
+    def __contains__(self, node):
+        try:
+            self[node]
+            return True
+        except KeyError:
+            return False
+
+    def items(self):
+        return zip(self.ids.tolist(), self.scores.tolist())
+
+    def values(self):
+        return self.scores.tolist()
+
+    def to_dict(self) -> dict:
+        return dict(zip(self.ids.tolist(), self.scores.tolist()))
+
+    def __eq__(self, other):
+        if isinstance(other, RankMap):
+            return np.array_equal(self.ids, other.ids) and np.array_equal(self.scores,
+                                                                           other.scores)
+        if isinstance(other, Mapping):
+            return self.to_dict() == dict(other.items())
+        return NotImplemented
+
+    def __repr__(self):
+        return f"RankMap(nodes={len(self)})"
+
+
+def pagerank(g, damping: float = 0.85, iterations: int = 10,
+             workers: int | None = None) -> RankMap:
+    """Damped power iteration, fp64, uniform start and dangling redistribution."""
+    if not 0.0 < damping < 1.0:
+        raise ValueError(f"damping must be in (0, 1), got {damping}")
+    if iterations < 1:
+        raise ValueError(f"iterations must be >= 1, got {iterations}")
+    if g.node_count == 0:
+        raise ValueError("pagerank needs a non-empty graph")
+    resolve_workers(workers)
+    dg = upload(g)
+    scores = _native.pagerank(dg.handle, dg.node_count, damping, iterations)
+    ids = dg.csr().ids if dg._host is not None else _ids_only(dg)
+    return RankMap(ids, scores)
+
+
+def _ids_only(dg: DeviceGraph) -> np.ndarray:
+    ids = np.empty(dg.node_count, dtype=np.int64)
+    if ids.size:
+        _native.check(_native.load().gt_graph_export(dg.handle, ids.ctypes.data, None, None,
+                                                     None, None), "gt_graph_export")
+    ids.flags.writeable = False
+    return ids
+
+
+def pagerank_device(g: DeviceGraph, damping: float, iterations: int, out_ptr: int) -> None:
+    """Scores straight into a device buffer of N doubles (no host copy)."""
+    _native.pagerank(g.handle, g.node_count, damping, iterations, out_ptr=out_ptr)
+
+
+def triangle_count(g, workers: int | None = None) -> int:
+    """Unordered mutually adjacent triples of the symmetrised graph."""
+    resolve_workers(workers)
+    if g.node_count == 0:
+        return 0
+    dg = upload(g)
+    return _native.triangles(dg.handle)

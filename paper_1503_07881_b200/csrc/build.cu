@@ -1,0 +1,543 @@
+// build.cu — ToGraph on the device: edge table -> out-CSR + in-CSR.
+//
+// Reference algorithm (convert.py:128-175): dense ids by np.unique
+// (convert.py:45-59), pack (src,dst) into a 64-bit key (convert.py:62-63),
+// sort + drop adjacent duplicates (convert.py:71-80), re-sort by (dst,src)
+// for the in-pool (convert.py:150-151), bincount/cumsum offsets
+// (convert.py:154-157), scatter into per-node pools (convert.py:92-125).
+//
+// Device pipeline (one stream, three small host syncs for sizes):
+//   minmax_kernel      16 B/row   id range -> dense or sparse id map
+//   presence_kernel    16 B/row   1 bit per id in the range (dense path)
+//   word_prefix_kernel W*8 B      popcount prefix -> rank of every present id
+//   ids_kernel         W*8 + 8N   sorted distinct ids
+//   pack_kernel        24 B/row   key = rank(src)<<k | rank(dst), k = ceil(log2 N),
+//                                 + digit histograms of every radix pass
+//   radix_sort         16 B/row/pass over 2k bits
+//   segment<dedupe>    8R + 12E + 8N  drop duplicate keys, out_adj, out_off,
+//                                 in-keys (dst<<k|src) + their digit histograms
+//   radix_sort         16 B/edge/pass over the k dst bits only (stable:
+//                                 src stays ascending within each dst)
+//   segment<plain>     8E + 4E + 8N   in_adj, in_off
+// Sparse ids (range wider than 32 ids per row) take the sort-unique path of
+// convert.py:59 instead: radix sort of the 2R ids + unique + binary search.
+#include "graph.cuh"
+#include "radix_sort.cuh"
+#include "segment.cuh"
+
+#include <algorithm>
+#include <cstring>
+
+namespace gtd {
+
+using gt::SortPlan;
+
+__global__ void __launch_bounds__(256) minmax_kernel(const int64_t* __restrict__ src,
+                                                     const int64_t* __restrict__ dst, int64_t n,
+                                                     long long* __restrict__ out) {
+  __shared__ long long smin[8], smax[8];
+  long long mn = LLONG_MAX, mx = LLONG_MIN;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long a = ld_stream_s64(src + i), b = ld_stream_s64(dst + i);
+    mn = min(mn, min(a, b));
+    mx = max(mx, max(a, b));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { smin[w] = mn; smax[w] = mx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < int(blockDim.x >> 5); ++i) { mn = min(mn, smin[i]); mx = max(mx, smax[i]); }
+    atomicMin(&out[0], mn);
+    atomicMax(&out[1], mx);
+  }
+}
+
+// Rank map word: presence bits of 32 consecutive ids + number of present ids
+// below the word (exclusive popcount prefix).
+__device__ __forceinline__ void mark_present(uint2* __restrict__ words, uint64_t off) {
+  unsigned int* p = &words[off >> 5].x;
+  const unsigned int bit = 1u << (off & 31);
+  if ((*reinterpret_cast<volatile unsigned int*>(p) & bit) == 0) atomicOr(p, bit);
+}
+
+__global__ void __launch_bounds__(256) presence_kernel(const int64_t* __restrict__ src,
+                                                       const int64_t* __restrict__ dst, int64_t n,
+                                                       int64_t lo, uint2* __restrict__ words) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    mark_present(words, uint64_t(ld_stream_s64(src + i)) - uint64_t(lo));
+    mark_present(words, uint64_t(ld_stream_s64(dst + i)) - uint64_t(lo));
+  }
+}
+
+// Blocked exclusive popcount scan over the rank-map words (16 words/thread).
+__global__ void __launch_bounds__(256) word_prefix_kernel(uint2* __restrict__ words, int64_t nw,
+                                                          uint64_t* __restrict__ status,
+                                                          uint32_t* __restrict__ counter,
+                                                          uint32_t epoch,
+                                                          int64_t* __restrict__ total_out) {
+  __shared__ uint32_t s_tile;
+  __shared__ int64_t s_scan[8];
+  __shared__ uint64_t s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+  __syncthreads();
+  const int tile = int(s_tile);
+  const int64_t first = (int64_t(tile) * 256 + threadIdx.x) * 16;
+  uint32_t c[16];
+  int64_t sum = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    c[j] = (first + j < nw) ? __popc(words[first + j].x) : 0u;
+    sum += c[j];
+  }
+  int64_t tot;
+  int64_t ex = block_excl_scan_256<int64_t>(sum, s_scan, tot);
+  if (threadIdx.x == 0) s_excl = lookback_single(status, tile, epoch, uint64_t(tot));
+  __syncthreads();
+  int64_t run = int64_t(s_excl) + ex;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (first + j < nw) words[first + j].y = uint32_t(run);
+    run += c[j];
+  }
+  if (first <= nw - 1 && nw - 1 < first + 16) *total_out = run;  // thread holding the last word
+}
+
+__global__ void __launch_bounds__(256) ids_kernel(const uint2* __restrict__ words, int64_t nw,
+                                                  int64_t lo, int64_t* __restrict__ ids) {
+  const int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (w >= nw) return;
+  uint2 v = words[w];
+  uint32_t bits = v.x;
+  int64_t pos = v.y;
+  while (bits) {
+    const int b = __ffs(bits) - 1;
+    bits &= bits - 1;
+    ids[pos++] = lo + (w << 5) + b;
+  }
+}
+
+__device__ __forceinline__ uint32_t rank_dense(const uint2* __restrict__ words, int64_t x,
+                                               int64_t lo) {
+  const uint64_t off = uint64_t(x) - uint64_t(lo);
+  const uint2 w = words[off >> 5];
+  return w.y + __popc(w.x & ((1u << (off & 31)) - 1u));
+}
+
+__device__ __forceinline__ uint32_t rank_search(const int64_t* __restrict__ ids, int64_t n,
+                                                int64_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (ids[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return uint32_t(lo);
+}
+
+template <bool DENSE>
+__global__ void __launch_bounds__(256) pack_kernel(const int64_t* __restrict__ src,
+                                                   const int64_t* __restrict__ dst, int64_t n,
+                                                   int64_t lo, const uint2* __restrict__ words,
+                                                   const int64_t* __restrict__ ids, int64_t n_ids,
+                                                   int kbits, SortPlan plan,
+                                                   unsigned long long* __restrict__ hist,
+                                                   uint64_t* __restrict__ keys) {
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
+  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t a = ld_stream_s64(src + i), b = ld_stream_s64(dst + i);
+    uint32_t ra, rb;
+    if (DENSE) {
+      ra = rank_dense(words, a, lo);
+      rb = rank_dense(words, b, lo);
+    } else {
+      ra = rank_search(ids, n_ids, a);
+      rb = rank_search(ids, n_ids, b);
+    }
+    const uint64_t key = (uint64_t(ra) << kbits) | rb;
+    keys[i] = key;
+    plan_hist_add(sh, plan, key);
+  }
+  __syncthreads();
+  plan_hist_flush(sh, plan, hist);
+}
+
+// Sparse path: ids shifted to unsigned offsets from lo, for a sort of 2R keys.
+__global__ void __launch_bounds__(256) idkeys_kernel(const int64_t* __restrict__ src,
+                                                     const int64_t* __restrict__ dst, int64_t n,
+                                                     int64_t lo, SortPlan plan,
+                                                     unsigned long long* __restrict__ hist,
+                                                     uint64_t* __restrict__ keys) {
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
+  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t a = uint64_t(ld_stream_s64(src + i)) - uint64_t(lo);
+    const uint64_t b = uint64_t(ld_stream_s64(dst + i)) - uint64_t(lo);
+    keys[i] = a;
+    keys[n + i] = b;
+    plan_hist_add(sh, plan, a);
+    plan_hist_add(sh, plan, b);
+  }
+  __syncthreads();
+  plan_hist_flush(sh, plan, hist);
+}
+
+// Sparse path: sorted id offsets -> distinct ids (lo + offset).
+__global__ void __launch_bounds__(256) unique_kernel(const uint64_t* __restrict__ keys, int64_t n,
+                                                     int64_t lo, int64_t* __restrict__ ids,
+                                                     uint64_t* __restrict__ status,
+                                                     uint32_t* __restrict__ counter,
+                                                     uint32_t epoch,
+                                                     int64_t* __restrict__ total_out) {
+  __shared__ uint32_t s_warp[8];
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_excl;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(counter, 1u);
+  __syncthreads();
+  const int tile = int(s_tile);
+  const int64_t wbase = int64_t(tile) * SEG_TILE + int64_t(warp) * 32 * SEG_KPT;
+  uint64_t k[SEG_KPT];
+  uint32_t keep_bits = 0, before[SEG_KPT], run = 0;
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int i = 0; i < SEG_KPT; ++i) {
+    const int64_t idx = wbase + i * 32 + lane;
+    k[i] = idx < n ? keys[idx] : 0ull;
+    const bool keep = idx < n && (idx == 0 || keys[idx - 1] != k[i]);
+    keep_bits |= uint32_t(keep) << i;
+    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+    before[i] = run + __popc(bal & lt);
+    run += __popc(bal);
+  }
+  if (lane == 0) s_warp[warp] = run;
+  __syncthreads();
+  uint32_t wpre = 0, tcount = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    const uint32_t c = s_warp[w];
+    if (w < warp) wpre += c;
+    tcount += c;
+  }
+  if (tid == 0) {
+    s_excl = lookback_single(status, tile, epoch, tcount);
+    if (int64_t(tile) == (n - 1) / SEG_TILE) *total_out = int64_t(s_excl) + tcount;
+  }
+  __syncthreads();
+  const int64_t base = int64_t(s_excl) + wpre;
+#pragma unroll
+  for (int i = 0; i < SEG_KPT; ++i)
+    if ((keep_bits >> i) & 1u) ids[base + before[i]] = lo + int64_t(k[i]);
+}
+
+__global__ void __launch_bounds__(256) gather_ids_kernel(const int32_t* __restrict__ adj, int64_t n,
+                                                         const int64_t* __restrict__ ids,
+                                                         int64_t* __restrict__ out) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = ids[adj[i]];
+}
+
+}  // namespace gtd
+
+namespace gt {
+
+static int grid_for(int64_t n, int per_thread = 1) {
+  const int64_t want = ceil_div64(n, 256LL * per_thread);
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(ctx().sm_count) * 8)));
+}
+
+static int64_t read_i64(const int64_t* d) {
+  int64_t h = 0;
+  d2h(&h, d, sizeof h);
+  sync();
+  return h;
+}
+
+static gt_graph* empty_graph() {
+  gt_graph* g = new gt_graph();
+  g->out_off = dalloc_n<int64_t>(1);
+  g->in_off = dalloc_n<int64_t>(1);
+  GT_CUDA(cudaMemsetAsync(g->out_off, 0, 8, ctx().stream));
+  GT_CUDA(cudaMemsetAsync(g->in_off, 0, 8, ctx().stream));
+  sync();
+  return g;
+}
+
+void graph_free(gt_graph* g) {
+  if (!g) return;
+  dfree(g->ids);
+  dfree(g->out_off);
+  dfree(g->out_adj);
+  dfree(g->in_off);
+  dfree(g->in_adj);
+  delete g;
+}
+
+gt_graph* build_csr(const int64_t* src, const int64_t* dst, int64_t rows, const int64_t* extra,
+                    int64_t n_extra, bool on_device) {
+  require_init();
+  if (rows < 0 || n_extra < 0) fail(GT_EINVAL, "rows must be >= 0");
+  if (n_extra > 0 && !extra) fail(GT_EINVAL, "extra node ids must not be NULL");
+  if (rows == 0 && n_extra == 0) return empty_graph();
+  cudaStream_t s = ctx().stream;
+
+  if (!on_device) {
+    int64_t* cols = ws_n<int64_t>(WS_COLS, size_t(2) * rows + size_t(n_extra));
+    Phase ph("build.h2d", 16.0 * rows + 8.0 * n_extra);
+    h2d(cols, src, size_t(rows) * 8);
+    h2d(cols + rows, dst, size_t(rows) * 8);
+    h2d(cols + 2 * rows, extra, size_t(n_extra) * 8);
+    src = cols;
+    dst = cols + rows;
+    extra = cols + 2 * rows;
+  }
+
+  gt_graph* g = new gt_graph();
+  try {
+    int64_t* small = ws_n<int64_t>(WS_SMALL, 16);  // [0]=min [1]=max [2]=N [3]=E
+    {
+      long long init[2] = {LLONG_MAX, LLONG_MIN};
+      h2d(small, init, sizeof init);
+      Phase ph("build.minmax", 16.0 * rows);
+      if (rows)
+        GT_LAUNCH(gtd::minmax_kernel, grid_for(rows, 4), 256, 0, src, dst, rows,
+                  reinterpret_cast<long long*>(small));
+      if (n_extra)
+        GT_LAUNCH(gtd::minmax_kernel, grid_for(n_extra, 4), 256, 0, extra, extra, n_extra,
+                  reinterpret_cast<long long*>(small));
+    }
+    int64_t mm[2];
+    d2h(mm, small, sizeof mm);
+    sync();
+    const int64_t lo = mm[0], hi = mm[1];
+    const uint64_t span = uint64_t(hi) - uint64_t(lo);  // width - 1, no overflow
+    // Dense rank map when its 8 bytes per 32 ids cost no more than one column.
+    const bool dense = span < (uint64_t(1) << 36) &&
+                       (span + 1) <= std::max<uint64_t>(uint64_t(1) << 26, uint64_t(rows) * 32);
+
+    uint2* words = nullptr;
+    int64_t nw = 0;
+    int64_t n_nodes = 0;
+    const size_t key_cap = dense ? size_t(rows) : size_t(2) * (rows + n_extra);
+    uint64_t* ka = ws_n<uint64_t>(WS_KEYS_A, key_cap);
+    uint64_t* kb = ws_n<uint64_t>(WS_KEYS_B, key_cap);
+    uint32_t* counters = ws_n<uint32_t>(WS_COUNTERS, 64);
+
+    if (dense) {
+      nw = int64_t((span + 1 + 31) / 32);
+      words = ws_n<uint2>(WS_RANKMAP, size_t(nw));
+      GT_CUDA(cudaMemsetAsync(words, 0, size_t(nw) * sizeof(uint2), s));
+      {
+        Phase ph("build.presence", 16.0 * rows);
+        if (rows)
+          GT_LAUNCH(gtd::presence_kernel, grid_for(rows, 4), 256, 0, src, dst, rows, lo, words);
+        if (n_extra)
+          GT_LAUNCH(gtd::presence_kernel, grid_for(n_extra, 4), 256, 0, extra, extra, n_extra, lo,
+                    words);
+      }
+      {
+        Phase ph("build.rank_prefix", 16.0 * nw);
+        const int64_t tiles = ceil_div64(nw, 256 * 16);
+        uint64_t* status = ws_n<uint64_t>(WS_LOOKBACK, size_t(tiles) * 256);
+        GT_CUDA(cudaMemsetAsync(counters + 16, 0, 4, s));
+        GT_LAUNCH(gtd::word_prefix_kernel, static_cast<int>(tiles), 256, 0, words, nw, status,
+                  counters + 16, next_epoch(), small + 2);
+      }
+      n_nodes = read_i64(small + 2);
+      if (n_nodes >= (int64_t(1) << 31))
+        fail(GT_ECAPACITY, "graph has >= 2^31 distinct node ids");
+      g->ids = dalloc_n<int64_t>(n_nodes);
+      {
+        Phase ph("build.ids", 8.0 * nw + 8.0 * n_nodes);
+        GT_LAUNCH(gtd::ids_kernel, ceil_div(nw, 256), 256, 0, words, nw, lo, g->ids);
+      }
+    } else {
+      // Sort-unique of the 2R ids (convert.py:59 searchsorted analogue).
+      const int64_t m = 2 * (rows + n_extra);
+      SortPlan idplan = make_plan(0, 64 - __builtin_clzll(span | 1));
+      SortHist hh = sort_hist_begin(0);
+      {
+        Phase ph("build.idkeys", 32.0 * (rows + n_extra));
+        if (rows)
+          GT_LAUNCH(gtd::idkeys_kernel, grid_for(rows, 4), 256, 0, src, dst, rows, lo, idplan,
+                    hh.hist, ka);
+        if (n_extra)
+          GT_LAUNCH(gtd::idkeys_kernel, grid_for(n_extra, 4), 256, 0, extra, extra, n_extra, lo,
+                    idplan, hh.hist, ka + 2 * rows);
+      }
+      uint64_t* sorted = radix_sort(ka, kb, m, idplan, hh, "build.id_sort");
+      int64_t* tmp_ids = reinterpret_cast<int64_t*>(sorted == ka ? kb : ka);
+      {
+        Phase ph("build.unique", 8.0 * m);
+        const int64_t tiles = ceil_div64(m, gtd::SEG_TILE);
+        uint64_t* status = ws_n<uint64_t>(WS_LOOKBACK, size_t(tiles) * 256);
+        GT_CUDA(cudaMemsetAsync(counters + 17, 0, 4, s));
+        GT_LAUNCH(gtd::unique_kernel, static_cast<int>(tiles), 256, 0, sorted, m, lo, tmp_ids,
+                  status, counters + 17, next_epoch(), small + 2);
+      }
+      n_nodes = read_i64(small + 2);
+      if (n_nodes >= (int64_t(1) << 31))
+        fail(GT_ECAPACITY, "graph has >= 2^31 distinct node ids");
+      g->ids = dalloc_n<int64_t>(n_nodes);
+      GT_CUDA(cudaMemcpyAsync(g->ids, tmp_ids, size_t(n_nodes) * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    g->n = n_nodes;
+    const int kb_bits = bits_for(n_nodes);
+    g->kbits = kb_bits;
+    if (rows == 0) {  // isolated nodes only
+      g->out_off = dalloc_n<int64_t>(n_nodes + 1);
+      g->in_off = dalloc_n<int64_t>(n_nodes + 1);
+      GT_CUDA(cudaMemsetAsync(g->out_off, 0, size_t(n_nodes + 1) * 8, s));
+      GT_CUDA(cudaMemsetAsync(g->in_off, 0, size_t(n_nodes + 1) * 8, s));
+      sync();
+      return g;
+    }
+
+    // ---- out pass: pack -> sort (src,dst) -> dedupe/out-CSR/in-keys --------
+    SortPlan out_plan = make_plan(0, 2 * kb_bits);
+    SortHist ho = sort_hist_begin(0);
+    {
+      Phase ph("build.pack", 24.0 * rows);
+      if (dense)
+        GT_LAUNCH(gtd::pack_kernel<true>, grid_for(rows, 4), 256, 0, src, dst, rows, lo, words,
+                  (const int64_t*)nullptr, int64_t(0), kb_bits, out_plan, ho.hist, ka);
+      else
+        GT_LAUNCH(gtd::pack_kernel<false>, grid_for(rows, 4), 256, 0, src, dst, rows, lo,
+                  (const uint2*)nullptr, g->ids, n_nodes, kb_bits, out_plan, ho.hist, ka);
+    }
+    uint64_t* sorted = radix_sort(ka, kb, rows, out_plan, ho, "build.out_sort");
+    uint64_t* other = sorted == ka ? kb : ka;
+
+    g->out_adj = dalloc_n<int32_t>(rows);  // E <= rows; exact E known after dedupe
+    g->out_off = dalloc_n<int64_t>(n_nodes + 1);
+    SortPlan in_plan = make_plan(kb_bits, 2 * kb_bits);
+    SortHist hi_ = sort_hist_begin(1);
+    {
+      Phase ph("build.dedupe", 8.0 * rows);
+      const int64_t tiles = ceil_div64(rows, gtd::SEG_TILE);
+      uint64_t* status = ws_n<uint64_t>(WS_LOOKBACK, size_t(tiles) * 256);
+      GT_CUDA(cudaMemsetAsync(counters + 18, 0, 4, s));
+      GT_LAUNCH(gtd::segment_kernel<true>, static_cast<int>(tiles), 256, 0, sorted, rows, kb_bits,
+                n_nodes, g->out_adj, g->out_off, other, in_plan, hi_.hist, status, counters + 18,
+                next_epoch(), small + 3);
+    }
+    const int64_t n_edges = read_i64(small + 3);
+    g->e = n_edges;
+    profile_add_bytes("build.dedupe", 12.0 * n_edges + 8.0 * (n_nodes + 1));
+
+    // ---- in pass: stable sort of in-keys by dst bits -> in-CSR -------------
+    uint64_t* in_sorted = radix_sort(other, sorted, n_edges, in_plan, hi_, "build.in_sort");
+    g->in_adj = dalloc_n<int32_t>(n_edges);
+    g->in_off = dalloc_n<int64_t>(n_nodes + 1);
+    {
+      Phase ph("build.in_segment", 12.0 * n_edges + 8.0 * n_nodes);
+      const int64_t tiles = ceil_div64(n_edges, gtd::SEG_TILE);
+      GT_LAUNCH(gtd::segment_kernel<false>, static_cast<int>(tiles), 256, 0, in_sorted, n_edges,
+                kb_bits, n_nodes, g->in_adj, g->in_off, (uint64_t*)nullptr, SortPlan(),
+                (unsigned long long*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr, 0u,
+                (int64_t*)nullptr);
+    }
+    sync();
+    return g;
+  } catch (...) {
+    graph_free(g);
+    throw;
+  }
+}
+
+void graph_export(const gt_graph* g, int64_t* ids, int64_t* out_off, int64_t* out_adj,
+                  int64_t* in_off, int64_t* in_adj) {
+  require_init();
+  if (!g) fail(GT_EINVAL, "null graph");
+  if (ids && g->n) d2h(ids, g->ids, size_t(g->n) * 8);
+  if (out_off) d2h(out_off, g->out_off, size_t(g->n + 1) * 8);
+  if (in_off) d2h(in_off, g->in_off, size_t(g->n + 1) * 8);
+  if ((out_adj || in_adj) && g->e) {
+    int64_t* tmp = ws_n<int64_t>(WS_TMP0, size_t(g->e));
+    if (out_adj) {
+      GT_LAUNCH(gtd::gather_ids_kernel, grid_for(g->e, 4), 256, 0, g->out_adj, g->e, g->ids, tmp);
+      d2h(out_adj, tmp, size_t(g->e) * 8);
+      sync();
+    }
+    if (in_adj) {
+      GT_LAUNCH(gtd::gather_ids_kernel, grid_for(g->e, 4), 256, 0, g->in_adj, g->e, g->ids, tmp);
+      d2h(in_adj, tmp, size_t(g->e) * 8);
+    }
+  }
+  sync();
+}
+
+}  // namespace gt
+
+using namespace gt;
+
+extern "C" {
+
+int gt_build_csr(const int64_t* src, const int64_t* dst, int64_t rows, int cols_are_device,
+                 gt_graph** out) {
+  GT_API_BEGIN
+  if (!out) fail(GT_EINVAL, "out must not be NULL");
+  *out = nullptr;
+  if (rows > 0 && (!src || !dst)) fail(GT_EINVAL, "src/dst must not be NULL");
+  *out = build_csr(src, dst, rows, nullptr, 0, cols_are_device != 0);
+  GT_API_END
+}
+
+int gt_build_csr_nodes(const int64_t* src, const int64_t* dst, int64_t rows, const int64_t* nodes,
+                       int64_t n_nodes, int cols_are_device, gt_graph** out) {
+  GT_API_BEGIN
+  if (!out) fail(GT_EINVAL, "out must not be NULL");
+  *out = nullptr;
+  if (rows > 0 && (!src || !dst)) fail(GT_EINVAL, "src/dst must not be NULL");
+  *out = build_csr(src, dst, rows, nodes, n_nodes, cols_are_device != 0);
+  GT_API_END
+}
+
+int gt_graph_sizes(const gt_graph* g, int64_t* n_nodes, int64_t* n_edges) {
+  GT_API_BEGIN
+  if (!g) fail(GT_EINVAL, "null graph");
+  if (n_nodes) *n_nodes = g->n;
+  if (n_edges) *n_edges = g->e;
+  GT_API_END
+}
+
+int gt_graph_export(const gt_graph* g, int64_t* h_ids, int64_t* h_out_off, int64_t* h_out_adj,
+                    int64_t* h_in_off, int64_t* h_in_adj) {
+  GT_API_BEGIN
+  graph_export(g, h_ids, h_out_off, h_out_adj, h_in_off, h_in_adj);
+  GT_API_END
+}
+
+int gt_graph_device_views(const gt_graph* g, const int64_t** d_ids, const int64_t** d_out_off,
+                          const int32_t** d_out_adj, const int64_t** d_in_off,
+                          const int32_t** d_in_adj) {
+  GT_API_BEGIN
+  if (!g) fail(GT_EINVAL, "null graph");
+  if (d_ids) *d_ids = g->ids;
+  if (d_out_off) *d_out_off = g->out_off;
+  if (d_out_adj) *d_out_adj = g->out_adj;
+  if (d_in_off) *d_in_off = g->in_off;
+  if (d_in_adj) *d_in_adj = g->in_adj;
+  GT_API_END
+}
+
+void gt_graph_free(gt_graph* g) {
+  try {
+    graph_free(g);
+  } catch (...) {
+  }
+}
+
+}  // extern "C"

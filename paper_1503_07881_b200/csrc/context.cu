@@ -1,0 +1,280 @@
+// context.cu — device/stream setup, error plumbing, scratch workspace,
+// launch accounting and per-phase CUDA-event timing for libgtb200.so.
+#include "common.cuh"
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+namespace gt {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  char buf[512];
+  snprintf(buf, sizeof buf, "%s failed: %s (%s:%d)", what, cudaGetErrorString(e), file, line);
+  fail(e == cudaErrorMemoryAllocation ? GT_ENOMEM : GT_ECUDA, buf);
+}
+
+static Context g_ctx;
+Context& ctx() { return g_ctx; }
+
+void require_init() {
+  if (g_ctx.stream == nullptr) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    if (gt_init(dev) != GT_OK) fail(GT_ENODEV, std::string("gt_init failed: ") + g_last_error);
+  }
+}
+
+void after_launch(const char* name) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "launch of %s failed: %s", name, cudaGetErrorString(e));
+    fail(GT_ECUDA, buf);
+  }
+}
+
+void* dalloc(size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 8;
+  cudaError_t e = cudaMallocAsync(&p, bytes, g_ctx.stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    char buf[256];
+    snprintf(buf, sizeof buf, "device allocation of %zu bytes failed: %s", bytes,
+             cudaGetErrorString(e));
+    fail(GT_ENOMEM, buf);
+  }
+  return p;
+}
+
+void dfree(void* p) {
+  if (p) cudaFreeAsync(p, g_ctx.stream);
+}
+
+struct SlotBuf { void* p = nullptr; size_t cap = 0; };
+static SlotBuf g_slots[WS_NSLOTS];
+
+void* ws_get(Slot s, size_t bytes) {
+  SlotBuf& b = g_slots[s];
+  if (b.cap < bytes) {
+    dfree(b.p);
+    size_t cap = bytes + bytes / 8;  // headroom so slightly larger inputs reuse
+    b.p = dalloc(cap);
+    b.cap = cap;
+    if (s == WS_LOOKBACK) GT_CUDA(cudaMemsetAsync(b.p, 0, cap, g_ctx.stream));
+  }
+  return b.p;
+}
+
+void ws_release_all() {
+  for (auto& b : g_slots) { dfree(b.p); b.p = nullptr; b.cap = 0; }
+}
+
+static uint32_t g_epoch = 0;
+uint32_t next_epoch() {
+  g_epoch = (g_epoch + 1) & 0x3FFFFFu;
+  if (g_epoch == 0) {  // wrapped: clear stale words so old epochs cannot alias
+    SlotBuf& b = g_slots[WS_LOOKBACK];
+    if (b.p) GT_CUDA(cudaMemsetAsync(b.p, 0, b.cap, g_ctx.stream));
+    g_epoch = 1;
+  }
+  return g_epoch;
+}
+
+void d2h(void* h, const void* d, size_t bytes) {
+  if (bytes) GT_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, g_ctx.stream));
+}
+void h2d(void* d, const void* h, size_t bytes) {
+  if (bytes) GT_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, g_ctx.stream));
+}
+void sync() { GT_CUDA(cudaStreamSynchronize(g_ctx.stream)); }
+
+// ---------------------------------------------------------------- profiling --
+struct PhaseStat {
+  std::string name;
+  double ms = 0.0;
+  int64_t launches = 0;
+  double bytes = 0.0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+};
+static std::vector<PhaseStat> g_phases;
+static std::vector<cudaEvent_t> g_event_pool;
+static std::mutex g_prof_mu;
+
+static cudaEvent_t get_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  GT_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+static int phase_index(const char* name) {
+  for (size_t i = 0; i < g_phases.size(); ++i)
+    if (g_phases[i].name == name) return static_cast<int>(i);
+  g_phases.push_back(PhaseStat{});
+  g_phases.back().name = name;
+  return static_cast<int>(g_phases.size() - 1);
+}
+
+static void resolve_pending() {
+  for (auto& p : g_phases) {
+    for (auto& ev : p.pending) {
+      GT_CUDA(cudaEventSynchronize(ev.second));
+      float ms = 0.f;
+      GT_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
+      p.ms += ms;
+      g_event_pool.push_back(ev.first);
+      g_event_pool.push_back(ev.second);
+    }
+    p.pending.clear();
+  }
+}
+
+Phase::Phase(const char* name, double bytes) {
+  if (!g_ctx.profiling) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  idx = phase_index(name);
+  g_phases[idx].bytes += bytes;
+  g_phases[idx].launches += 1;
+  start = get_event();
+  GT_CUDA(cudaEventRecord(start, g_ctx.stream));
+}
+
+void profile_add_bytes(const char* name, double bytes) {
+  if (!g_ctx.profiling) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_phases[phase_index(name)].bytes += bytes;
+}
+
+Phase::~Phase() {
+  if (idx < 0) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEvent_t end = get_event();
+  if (cudaEventRecord(end, g_ctx.stream) != cudaSuccess) return;
+  g_phases[idx].pending.emplace_back(start, end);
+}
+
+}  // namespace gt
+
+using namespace gt;
+
+extern "C" {
+
+int gt_init(int device) {
+  try {
+    Context& c = ctx();
+    if (c.stream != nullptr && c.device == device) return GT_OK;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      fail(GT_ENODEV, "no CUDA device visible (libgtb200 has no CPU fallback)");
+    }
+    if (device < 0 || device >= n) fail(GT_EINVAL, "device ordinal out of range");
+    GT_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    GT_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0) {
+      char buf[160];
+      snprintf(buf, sizeof buf, "device %d is sm_%d%d; libgtb200 is built for sm_100a only",
+               device, prop.major, prop.minor);
+      fail(GT_ENODEV, buf);
+    }
+    c.device = device;
+    c.sm_count = prop.multiProcessorCount;
+    c.l2_bytes = prop.l2CacheSize;
+    GT_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    GT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    GT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    return GT_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  }
+}
+
+const char* gt_version(void) { return "gtb200 0.1.0 (sm_100a)"; }
+
+void* gt_stream(void) {
+  try {
+    require_init();
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return nullptr;
+  }
+  return ctx().stream;
+}
+
+const char* gt_last_error(void) { return g_last_error.c_str(); }
+
+int gt_release_workspace(void) {
+  try {
+    if (ctx().stream == nullptr) return GT_OK;
+    ws_release_all();
+    sync();
+    return GT_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  }
+}
+
+int64_t gt_launch_count(void) { return g_launches.load(); }
+
+int gt_profile_enable(int on) {
+  ctx().profiling = on != 0;
+  return GT_OK;
+}
+
+int gt_profile_reset(void) {
+  try {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    resolve_pending();
+    for (auto& p : g_phases) { p.ms = 0; p.launches = 0; p.bytes = 0; }
+    return GT_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  }
+}
+
+int gt_profile_read(int cap, const char** names, double* total_ms, int64_t* launches,
+                    double* bytes) {
+  try {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    resolve_pending();
+    int n = 0;
+    for (auto& p : g_phases) {
+      if (p.launches == 0) continue;
+      if (n < cap) {
+        if (names) names[n] = p.name.c_str();
+        if (total_ms) total_ms[n] = p.ms;
+        if (launches) launches[n] = p.launches;
+        if (bytes) bytes[n] = p.bytes;
+      }
+      ++n;
+    }
+    return n;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return -e.code;
+  }
+}
+
+}  // extern "C"

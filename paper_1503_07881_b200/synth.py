@@ -1,0 +1,151 @@
+"""Deterministic synthetic edge tables (bench and test inputs).
+
+``random_edges`` keeps the reference's uniform generator semantics
+(``synth.py:20-29``: ``np.random.default_rng(seed).integers(0, n, size)`` for
+src then dst). ``rmat_edges`` is the R-MAT generator the BASELINE configs
+name; the reference has none, so it is defined here once and implemented
+twice — in numpy (this file, the oracle side) and in CUDA
+(``csrc/rmat.cu``, ``gt_rmat_generate``) — bit for bit identical. Every row
+depends only on its index, so any row range can be generated on its own.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+_U64 = np.uint64
+_SEED_SALT = 0x5851F42D4C957F2D
+_ROUND_SALT = 0xA0761D6478BD642F
+_TWO53 = 9007199254740992.0
+_MASK64 = (1 << 64) - 1
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    """splitmix64 finaliser on a uint64 array (wrapping arithmetic)."""
+    z = x + _U64(0x9E3779B97F4A7C15)
+    z = (z ^ (z >> _U64(30))) * _U64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> _U64(27))) * _U64(0x94D049BB133111EB)
+    return z ^ (z >> _U64(31))
+
+
+def _sm64_scalar(x: int) -> int:
+    return int(splitmix64(np.asarray([x & _MASK64], dtype=np.uint64))[0])
+
+
+@dataclass(frozen=True)
+class RmatSpec:
+    scale: int
+    rows: int
+    a: float = 0.57
+    b: float = 0.19
+    c: float = 0.19
+    seed: int = 1
+    permute: bool = False
+
+
+def _thresholds(a: float, b: float, c: float):
+    return int(a * _TWO53), int((a + b) * _TWO53), int((a + b + c) * _TWO53)
+
+
+def feistel_permute(x: np.ndarray, scale: int, key: int) -> np.ndarray:
+    """Keyed bijection of [0, 2^scale): 4-round Feistel, cycle-walked."""
+    h = (scale + 1) // 2
+    mh = _U64((1 << h) - 1)
+    limit = _U64(1 << scale)
+    rk = [_sm64_scalar(key ^ ((_ROUND_SALT * (r + 1)) & _MASK64)) for r in range(4)]
+    x = x.astype(np.uint64, copy=True)
+    todo = np.ones(x.shape[0], dtype=bool)
+    while True:
+        idx = np.nonzero(todo)[0]
+        if idx.size == 0:
+            return x
+        v = x[idx]
+        left, right = v >> _U64(h), v & mh
+        for r in range(4):
+            left, right = right, left ^ (splitmix64(right ^ _U64(rk[r])) & mh)
+        v = (left << _U64(h)) | right
+        x[idx] = v
+        todo[idx] = v >= limit
+
+
+def rmat_edges(scale: int, rows: int, a: float = 0.57, b: float = 0.19, c: float = 0.19,
+               seed: int = 1, permute: bool = False, start: int = 0,
+               chunk: int = 1 << 22):
+    """R-MAT rows [start, start+rows) as two int64 arrays (src, dst)."""
+    if scale < 1 or scale > 40:
+        raise ValueError("scale must be in [1, 40]")
+    key = _sm64_scalar(seed ^ _SEED_SALT)
+    ta, tab, tabc = (_U64(t) for t in _thresholds(a, b, c))
+    src = np.empty(rows, dtype=np.int64)
+    dst = np.empty(rows, dtype=np.int64)
+    for lo in range(0, rows, chunk):
+        hi = min(rows, lo + chunk)
+        e = np.arange(start + lo, start + hi, dtype=np.uint64)
+        base = _U64(key) + e * _U64(scale)
+        s = np.zeros(hi - lo, dtype=np.uint64)
+        d = np.zeros(hi - lo, dtype=np.uint64)
+        for level in range(scale):
+            u = splitmix64(base + _U64(level)) >> _U64(11)
+            sb = (u >= tab).astype(np.uint64)
+            db = (((u >= ta) & (u < tab)) | (u >= tabc)).astype(np.uint64)
+            s = (s << _U64(1)) | sb
+            d = (d << _U64(1)) | db
+        if permute:
+            s = feistel_permute(s, scale, key)
+            d = feistel_permute(d, scale, key)
+        src[lo:hi] = s.astype(np.int64)
+        dst[lo:hi] = d.astype(np.int64)
+    return src, dst
+
+
+def random_edges_arrays(n_nodes: int, n_edges: int, seed: int = 0):
+    """Uniform iid src/dst in [0, n_nodes) — synth.py:20-29 semantics."""
+    if n_nodes < 0 or n_edges < 0:
+        raise ValueError("sizes must be >= 0")
+    if n_nodes == 0 and n_edges > 0:
+        raise ValueError("cannot draw edges from an empty node range")
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, max(n_nodes, 1), size=n_edges, dtype=np.int64)
+    dst = rng.integers(0, max(n_nodes, 1), size=n_edges, dtype=np.int64)
+    return src, dst
+
+
+# BASELINE.json configs (C3 reuses the C2 table; C4's dense remap and C5's
+# 2B-row uniform table are generated on the device by bench.py).
+CONFIGS = {
+    "c1": RmatSpec(scale=17, rows=1_048_576, seed=1, permute=False),
+    "c2": RmatSpec(scale=22, rows=69_000_000, seed=2, permute=True),
+    "c4": RmatSpec(scale=26, rows=1_470_000_000, seed=3, permute=True),
+}
+
+
+def rmat_device(spec: RmatSpec, device: str = "cuda"):
+    """Generate an R-MAT table straight into HBM (torch int64 tensors)."""
+    import torch
+
+    from . import _native
+
+    src = torch.empty(spec.rows, dtype=torch.int64, device=device)
+    dst = torch.empty(spec.rows, dtype=torch.int64, device=device)
+    _native.rmat_generate(spec.scale, spec.rows, spec.a, spec.b, spec.c, spec.seed,
+                          spec.permute, src.data_ptr(), dst.data_ptr())
+    return src, dst
+
+
+def random_edges(n_nodes: int, n_edges: int, seed: int = 0):
+    """ColumnTable of uniform random edges (reference synth.random_edges)."""
+    from .tables import INT, ColumnTable, Schema
+
+    src, dst = random_edges_arrays(n_nodes, n_edges, seed)
+    return ColumnTable(Schema([("src", INT), ("dst", INT)]), [src, dst])
+
+
+def rmat_table(spec: RmatSpec):
+    """ColumnTable of an R-MAT spec generated on the host (numpy)."""
+    from .tables import INT, ColumnTable, Schema
+
+    src, dst = rmat_edges(spec.scale, spec.rows, spec.a, spec.b, spec.c, spec.seed,
+                          spec.permute)
+    return ColumnTable(Schema([("src", INT), ("dst", INT)]), [src, dst])

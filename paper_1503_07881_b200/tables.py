@@ -1,0 +1,187 @@
+"""Column tables for the ToGraph path: schema-typed int64 columns that can
+live in host memory (numpy) or in HBM (torch CUDA tensors).
+
+Mirrors the parts of the reference's ``tables.py`` the path touches:
+``Schema`` (tables.py:44-90, incl. ``parse``), ``ColumnTable.column`` /
+``n_rows`` (tables.py:128-186) and ``load_tsv`` (tables.py:246-284: headerless
+UTF-8 TSV, exact field count, ``ParseError`` carrying line and column).
+``ColumnTable.to_device()`` is new: it makes the int columns device-resident
+once, so every later ToGraph reads them straight from HBM.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .errors import ParseError, SchemaError, TypeMismatchError, UnknownColumnError
+
+INT, FLOAT, STRING = "int", "float", "str"
+_TYPES = (INT, FLOAT, STRING)
+
+
+class Schema:
+    """Ordered (name, type) pairs; types are int, float or str."""
+
+    def __init__(self, columns):
+        cols = [(str(n), t) for n, t in columns]
+        if not cols:
+            raise SchemaError("schema must have at least one column")
+        names = [n for n, _ in cols]
+        if len(set(names)) != len(names):
+            raise SchemaError(f"duplicate column names in {names}")
+        for name, typ in cols:
+            if not name:
+                raise SchemaError("column names must be non-empty")
+            if typ not in _TYPES:
+                raise SchemaError(f"unknown column type {typ!r} for {name!r}")
+        self.columns = cols
+        self._index = {n: i for i, n in enumerate(names)}
+
+    def __len__(self):
+        return len(self.columns)
+
+    def __eq__(self, other):
+        return isinstance(other, Schema) and self.columns == other.columns
+
+    def __repr__(self):
+        return "Schema(%s)" % ", ".join(f"{n}:{t}" for n, t in self.columns)
+
+    @property
+    def names(self):
+        return [n for n, _ in self.columns]
+
+    def index_of(self, name: str) -> int:
+        try:
+            return self._index[name]
+        except KeyError:
+            raise UnknownColumnError(f"no column named {name!r} (have {self.names})") from None
+
+    def type_of(self, name: str) -> str:
+        return self.columns[self.index_of(name)][1]
+
+    @classmethod
+    def parse(cls, text: str) -> "Schema":
+        """'src:int,dst:int' -> Schema."""
+        cols = []
+        for part in text.split(","):
+            name, _, typ = part.partition(":")
+            cols.append((name.strip(), typ.strip()))
+        return cls(cols)
+
+
+def _is_device(col) -> bool:
+    return getattr(col, "is_cuda", False) or hasattr(col, "__cuda_array_interface__")
+
+
+def _length(col) -> int:
+    return int(col.shape[0])
+
+
+class ColumnTable:
+    """Schema-typed columns of equal length (host numpy or device tensors)."""
+
+    def __init__(self, schema: Schema, columns, pool=None):
+        if len(columns) != len(schema):
+            raise SchemaError("column count does not match schema")
+        cols = [c if _is_device(c) else np.asarray(c) for c in columns]
+        lengths = {_length(c) for c in cols}
+        if len(lengths) > 1:
+            raise SchemaError(f"ragged column lengths {sorted(lengths)}")
+        self.schema = schema
+        self.columns = cols
+        self.pool = pool if pool is not None else []
+
+    @property
+    def n_rows(self) -> int:
+        return _length(self.columns[0]) if self.columns else 0
+
+    def column(self, name: str):
+        return self.columns[self.schema.index_of(name)]
+
+    def is_device_resident(self, name: str) -> bool:
+        return _is_device(self.column(name))
+
+    def to_device(self, device="cuda") -> "ColumnTable":
+        """Copy of the table whose int columns live in HBM (torch int64)."""
+        import torch
+
+        cols = []
+        for (name, typ), col in zip(self.schema.columns, self.columns):
+            if typ == INT and not _is_device(col):
+                col = torch.from_numpy(np.ascontiguousarray(col, dtype=np.int64)).to(device)
+            cols.append(col)
+        return ColumnTable(self.schema, cols, pool=self.pool)
+
+    def to_host(self) -> "ColumnTable":
+        cols = [c.cpu().numpy() if _is_device(c) else c for c in self.columns]
+        return ColumnTable(self.schema, cols, pool=self.pool)
+
+    def to_rows(self) -> list[tuple]:
+        host = self.to_host()
+        out = []
+        for i in range(self.n_rows):
+            row = []
+            for (_, typ), col in zip(self.schema.columns, host.columns):
+                v = col[i]
+                row.append(self.pool[int(v)] if typ == STRING else
+                           (int(v) if typ == INT else float(v)))
+            out.append(tuple(row))
+        return out
+
+    def memory_bytes(self) -> int:
+        return int(sum(c.nbytes if hasattr(c, "nbytes") else c.element_size() * c.numel()
+                       for c in self.columns))
+
+    def __repr__(self):
+        return f"ColumnTable({self.schema!r}, rows={self.n_rows})"
+
+
+def load_tsv(path, schema: Schema) -> ColumnTable:
+    """Headerless TSV, one row per line, fields per schema (tables.py:246-284)."""
+    n_cols = len(schema)
+    raw = [[] for _ in range(n_cols)]
+    pool: list[str] = []
+    codes: dict[str, int] = {}
+    with open(path, "r", encoding="utf-8") as fh:
+        for lineno, line in enumerate(fh, start=1):
+            fields = line.rstrip("\n").split("\t")
+            if len(fields) != n_cols:
+                raise ParseError(f"line {lineno}: expected {n_cols} fields, got {len(fields)}",
+                                 line=lineno)
+            for j, (name, typ) in enumerate(schema.columns):
+                field = fields[j]
+                if typ == STRING:
+                    code = codes.get(field)
+                    if code is None:
+                        code = codes[field] = len(pool)
+                        pool.append(field)
+                    raw[j].append(code)
+                    continue
+                conv = int if typ == INT else float
+                try:
+                    raw[j].append(conv(field))
+                except ValueError:
+                    kind = "an integer" if typ == INT else "a float"
+                    raise ParseError(f"line {lineno}, column {name!r}: {field!r} is not {kind}",
+                                     line=lineno, column=name) from None
+    arrays = [np.asarray(raw[j], dtype=np.float64 if t == FLOAT else np.int64)
+              for j, (_, t) in enumerate(schema.columns)]
+    return ColumnTable(schema, arrays, pool=pool)
+
+
+def save_tsv(table: ColumnTable, path) -> None:
+    """Inverse of load_tsv for int/float/str columns."""
+    rows = table.to_rows()
+    with open(path, "w", encoding="utf-8") as fh:
+        for row in rows:
+            parts = []
+            for v, (_, typ) in zip(row, table.schema.columns):
+                if typ == STRING and ("\t" in v or "\n" in v):
+                    raise TypeMismatchError(f"string value {v!r} contains a tab or newline")
+                parts.append(repr(v) if typ == FLOAT else str(v))
+            fh.write("\t".join(parts) + "\n")
+
+
+def edge_table(src, dst, names=("src", "dst")) -> ColumnTable:
+    """Two-int-column edge table from arrays (host or device)."""
+    return ColumnTable(Schema([(names[0], INT), (names[1], INT)]), [src, dst])

@@ -1,0 +1,68 @@
+"""Pin the CPU oracle against outputs of the real reference (CPU only).
+
+The fixtures were recorded by tests/golden/make_golden.py running the
+unmodified reference ``graphtables`` in the build container; here the
+restatement (oracle/reference_port.py, oracle/fast_oracle.c) must reproduce
+them exactly (CSR, triangles) and to 1e-12 (PageRank: same algorithm, same
+summation order).
+"""
+
+import numpy as np
+import pytest
+
+from helpers import assert_csr_equal, golden_c1, golden_cases, sha
+from oracle import reference_port as ref
+from paper_1503_07881_b200.synth import rmat_edges
+
+CASES = sorted(golden_cases())
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_build_matches_reference(name):
+    case = golden_cases()[name]
+    got = ref.build_csr(case["src"], case["dst"], workers=4)
+    assert_csr_equal(got, case, name)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_pagerank_matches_reference(name):
+    case = golden_cases()[name]
+    if case["ids"].shape[0] == 0:
+        pytest.skip("empty graph")
+    g = ref.build_csr(case["src"], case["dst"], workers=2)
+    pr = ref.pagerank_csr(g, 0.85, 10, workers=3)
+    assert np.max(np.abs(pr - case["pr"])) <= 1e-12
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_fast_triangle_oracle_matches_reference(name):
+    case = golden_cases()[name]
+    g = ref.build_csr(case["src"], case["dst"], workers=1)
+    assert ref.triangle_count_fast(g, threads=2) == int(case["tc"][0])
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if golden_cases()[n]["ids"].shape[0] <= 2000])
+def test_numpy_triangle_oracle_matches_reference(name):
+    case = golden_cases()[name]
+    g = ref.build_csr(case["src"], case["dst"], workers=1)
+    assert ref.triangle_count_csr(g, workers=2) == int(case["tc"][0])
+
+
+def test_c1_config_matches_reference():
+    """BASELINE config 0 (R-MAT s17, 1,048,576 rows, seed 1) end to end."""
+    gold = golden_c1()
+    src, dst = rmat_edges(17, 1_048_576, seed=1, permute=False)
+    assert sha(src) == str(gold["sha_src"]) and sha(dst) == str(gold["sha_dst"])
+    g = ref.build_csr(src, dst)
+    for f in ("ids", "out_off", "out_adj", "in_off", "in_adj"):
+        assert sha(getattr(g, f)) == str(gold[f"sha_{f}"]), f
+    pr = ref.pagerank_csr(g, 0.85, 10)
+    assert np.max(np.abs(pr - gold["pr"])) <= 1e-12
+    assert ref.triangle_count_fast(g) == int(gold["tc"][0])
+
+
+def test_parallel_sort_equals_np_sort():
+    rng = np.random.default_rng(0)
+    v = rng.integers(0, 1 << 40, size=300_000).astype(np.uint64)
+    for w in (1, 3, 8):
+        assert np.array_equal(ref.parallel_sort(v, w), np.sort(v))

@@ -1,0 +1,95 @@
+"""Triangle counting on the B200: exact vs the reference (golden), the cubic
+brute-force oracle (oracles.py:163-167) and the C restatement."""
+
+import numpy as np
+import pytest
+
+import paper_1503_07881_b200 as gt
+from helpers import cubic_triangles, golden_c1, golden_cases, random_digraph_edges
+from oracle import reference_port as ref
+from paper_1503_07881_b200.synth import CONFIGS, RmatSpec, rmat_device
+
+pytestmark = pytest.mark.gpu
+SPEC = gt.EdgeSpec("src", "dst")
+
+
+def build(src, dst):
+    return gt.table_to_graph(gt.edge_table(np.asarray(src, np.int64),
+                                           np.asarray(dst, np.int64)), SPEC)
+
+
+@pytest.mark.parametrize("name", sorted(golden_cases()))
+def test_matches_reference(name):
+    case = golden_cases()[name]
+    assert gt.triangle_count(build(case["src"], case["dst"])) == int(case["tc"][0])
+
+
+def test_c1_config_matches_reference():
+    src, dst = rmat_device(CONFIGS["c1"])
+    g = gt.table_to_graph(gt.edge_table(src, dst), SPEC)
+    assert gt.triangle_count(g) == int(golden_c1()["tc"][0])
+
+
+def test_known_answers():
+    k4 = [(a, b) for a in range(4) for b in range(4) if a < b]
+    assert gt.triangle_count(gt.from_edges(k4)) == 4
+    assert gt.triangle_count(gt.from_edges([(i, i + 1) for i in range(9)])) == 0
+    assert gt.triangle_count(gt.from_edges([(0, 0), (0, 1), (1, 2), (2, 0)])) == 1
+    assert gt.triangle_count(build([], [])) == 0
+    assert gt.triangle_count(build([5], [5])) == 0
+
+
+def test_direction_flips_do_not_change_count():
+    rng = np.random.default_rng(4)
+    src, dst = random_digraph_edges(rng, 40, 0.1)
+    base = gt.triangle_count(build(src, dst))
+    flip = rng.random(src.shape[0]) < 0.5
+    s2 = np.where(flip, dst, src)
+    d2 = np.where(flip, src, dst)
+    assert gt.triangle_count(build(s2, d2)) == base
+
+
+def test_random_vs_cubic_enumeration():
+    rng = np.random.default_rng(77)
+    for i in range(50):
+        n = int(rng.integers(2, 41)) if i % 2 else int(rng.integers(40, 129))
+        p = float(rng.uniform(0.05, 0.4)) if i % 2 else float(rng.uniform(0.01, 8 / n))
+        src, dst = random_digraph_edges(rng, n, p)
+        adj = np.zeros((n, n), dtype=bool)
+        adj[src, dst] = True
+        want = cubic_triangles(adj | adj.T)
+        got = gt.triangle_count(build(src, dst)) if src.size else 0
+        assert got == want
+
+
+def test_hub_heavy_graph_vs_oracle():
+    """Dense core (d+(u) beyond the shared-memory cap) + long tails."""
+    rng = np.random.default_rng(5)
+    core = rng.integers(0, 3000, size=(400_000, 2))
+    tail = rng.integers(0, 200_000, size=(300_000, 2))
+    e = np.concatenate([core, tail])
+    g = build(e[:, 0], e[:, 1])
+    want = ref.triangle_count_fast(ref.build_csr(e[:, 0], e[:, 1]))
+    assert gt.triangle_count(g) == want
+
+
+def test_c3_prefix_vs_oracle():
+    src, dst = rmat_device(RmatSpec(scale=22, rows=4_000_000, seed=2, permute=True))
+    g = gt.table_to_graph(gt.edge_table(src, dst), SPEC)
+    want = ref.triangle_count_fast(ref.build_csr(src.cpu().numpy(), dst.cpu().numpy()))
+    assert gt.triangle_count(g) == want
+
+
+def test_repeatable():
+    src, dst = rmat_device(RmatSpec(scale=18, rows=2_000_000, seed=9, permute=True))
+    g = gt.table_to_graph(gt.edge_table(src, dst), SPEC)
+    assert gt.triangle_count(g) == gt.triangle_count(g)
+
+
+@pytest.mark.slow
+def test_c3_full_vs_oracle():
+    src, dst = rmat_device(CONFIGS["c2"])
+    g = gt.table_to_graph(gt.edge_table(src, dst), SPEC)
+    h = g.csr()
+    want = ref.triangle_count_fast(ref.CSR(h.ids, h.out_off, h.out_adj, h.in_off, h.in_adj))
+    assert gt.triangle_count(g) == want
