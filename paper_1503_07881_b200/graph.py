@@ -210,7 +210,7 @@ class Graph(_GraphReadAPI):
         for n, rec in self._nodes.items():
             for vec in (rec.out_nbrs, rec.in_nbrs):
                 if vec.shape[0] > 1:
-                    assert bool(np.all(np.diff(vec) > 0)), f"unsorted vector at {n}"
+                    assert bool(np.all(vec[1:] > vec[:-1])), f"unsorted vector at {n}"
             total_out += rec.out_nbrs.shape[0]
             total_in += rec.in_nbrs.shape[0]
             for dst in rec.out_nbrs.tolist():
@@ -346,10 +346,10 @@ class DeviceGraph(_GraphReadAPI):
             if e > 1:
                 row_start = np.zeros(e, dtype=bool)
                 row_start[off[:-1][off[:-1] < e]] = True
-                inc = np.diff(adj) > 0
+                inc = adj[1:] > adj[:-1]  # no np.diff: int64 extremes overflow
                 assert bool(np.all(inc | row_start[1:])), "unsorted adjacency vector"
         if n > 1:
-            assert bool(np.all(np.diff(h.ids) > 0)), "node ids not strictly ascending"
+            assert bool(np.all(h.ids[1:] > h.ids[:-1])), "node ids not strictly ascending"
         src = np.repeat(h.ids, np.diff(h.out_off))
         dst_of_in = np.repeat(h.ids, np.diff(h.in_off))
         a = np.lexsort((h.out_adj, src))
