@@ -122,6 +122,17 @@ GT_API int gt_pagerank(const gt_graph* g, double damping, int iterations,
  * self-loops ignored; 0 for an empty graph (algorithms.py:100-101). */
 GT_API int gt_triangles(const gt_graph* g, int64_t* count);
 
+/* Degree-ordered orientation used by gt_triangles (algorithms.py:103-108),
+ * for parity tests: h_deg[N] = undirected degree |in ∪ out \ {i}| by dense
+ * index (graphs.py:163-167); h_rank[N] = position of node i in (degree, id)
+ * order (algorithms.py:104-106); the oriented CSR in RANK space, N+(r) = the
+ * higher-ranked neighbours of the node of rank r, ascending: h_off_p[N+1],
+ * h_adj_p[m] (m = undirected edge count, returned in *m; call once with
+ * h_adj_p = NULL to size it). Any output pointer may be NULL; GT_EINVAL for a
+ * graph without edges. */
+GT_API int gt_triangle_orientation(const gt_graph* g, int32_t* h_deg, int32_t* h_rank,
+                                   int64_t* h_off_p, int32_t* h_adj_p, int64_t* m);
+
 /* ---- synthetic inputs (bench / tests; no reference counterpart) --------- */
 
 /* R-MAT edge table generated on the device, bit-identical to the numpy

@@ -233,12 +233,9 @@ def undirected_dense(g: CSR):
     return und
 
 
-def triangle_count_csr(g: CSR, workers=None, und=None) -> int:
-    """algorithms.py:90-119 — one intersect1d per oriented edge."""
-    workers = resolve_workers(workers)
+def orientation_dense(g: CSR, und=None):
+    """algorithms.py:102-108 — undirected degree and higher(i) (id order)."""
     n = g.n
-    if n == 0:
-        return 0
     if und is None:
         und = undirected_dense(g)
     deg = np.asarray([u.shape[0] for u in und], dtype=np.int64)
@@ -246,6 +243,16 @@ def triangle_count_csr(g: CSR, workers=None, und=None) -> int:
     rank = np.empty(n, dtype=np.int64)
     rank[by_rank] = np.arange(n)
     higher = [u[rank[u] > rank[i]] for i, u in enumerate(und)]
+    return deg, higher
+
+
+def triangle_count_csr(g: CSR, workers=None, und=None) -> int:
+    """algorithms.py:90-119 — one intersect1d per oriented edge."""
+    workers = resolve_workers(workers)
+    n = g.n
+    if n == 0:
+        return 0
+    _, higher = orientation_dense(g, und)
 
     def count_range(a, b):
         total = 0

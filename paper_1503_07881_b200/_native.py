@@ -40,6 +40,7 @@ SIGNATURES = {
     "gt_graph_free": (None, [_VP]),
     "gt_pagerank": (ctypes.c_int, [_VP, ctypes.c_double, ctypes.c_int, _VP, ctypes.c_int]),
     "gt_triangles": (ctypes.c_int, [_VP, _I64P]),
+    "gt_triangle_orientation": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _I64P]),
     "gt_rmat_generate": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
                                         ctypes.c_int, _VP, _VP]),
@@ -183,6 +184,21 @@ def triangles(handle: int) -> int:
     c = ctypes.c_int64()
     check(lib.gt_triangles(handle, ctypes.byref(c)), "gt_triangles")
     return int(c.value)
+
+
+def triangle_orientation(handle: int, n: int):
+    """-> (deg[N], rank[N], off_p[N+1], adj_p[m]): the rank-space orientation."""
+    lib = ensure_init()
+    m = ctypes.c_int64()
+    deg = np.empty(n, dtype=np.int32)
+    rank = np.empty(n, dtype=np.int32)
+    off_p = np.empty(n + 1, dtype=np.int64)
+    check(lib.gt_triangle_orientation(handle, _ptr(deg), _ptr(rank), _ptr(off_p), None,
+                                      ctypes.byref(m)), "gt_triangle_orientation")
+    adj_p = np.empty(int(m.value), dtype=np.int32)
+    check(lib.gt_triangle_orientation(handle, None, None, None, _ptr(adj_p), ctypes.byref(m)),
+          "gt_triangle_orientation")
+    return deg, rank, off_p, adj_p
 
 
 def rmat_generate(scale, rows, a, b, c, seed, permute, src_ptr, dst_ptr):

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(256) digit_scan_kernel(const unsigned long lon
   base[q * 256 + threadIdx.x] = ex;
 }
 
-__global__ void __launch_bounds__(RS_THREADS, 2)
+__global__ void __launch_bounds__(RS_THREADS, 3)
     onesweep_kernel(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int64_t n,
                     int shift, int bits, const int64_t* __restrict__ digit_base,
                     uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter,
@@ -63,20 +63,18 @@ __global__ void __launch_bounds__(RS_THREADS, 2)
     k[i] = idx < n ? ld_stream_u64(in + idx) : ~0ull;
   }
 
-  // Warp-level multi-split: rank every key among equal digits of its warp.
+  // Warp-level multi-split: rank every key among the equal digits of its
+  // warp in lane order (stable). __match_any_sync finds the peers of a digit
+  // in one instruction; invalid tail keys match only each other (digit 256).
   uint32_t rank[RS_KPT];
   const unsigned lt = lanemask_lt();
 #pragma unroll
   for (int i = 0; i < RS_KPT; ++i) {
     const bool valid = (wbase + i * 32 + lane) < n;
-    const uint32_t d = uint32_t(k[i] >> shift) & mask;
-    uint32_t peers = __ballot_sync(0xffffffffu, valid);
-    for (int b = 0; b < bits; ++b) {
-      const bool bit = (d >> b) & 1u;
-      const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-      peers &= bit ? bal : ~bal;
-    }
-    const uint32_t before = s.whist[warp][d];
+    const uint32_t d = valid ? uint32_t(k[i] >> shift) & mask : 256u;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    uint32_t before = 0;
+    if (valid) before = s.whist[warp][d];
     rank[i] = before + __popc(peers & lt);
     const int leader = 31 - __clz(peers);
     __syncwarp();
@@ -97,8 +95,8 @@ __global__ void __launch_bounds__(RS_THREADS, 2)
     }
     const uint32_t tile_cnt = run;
     uint64_t* st = status + int64_t(tile) * 256 + d;
-    if (tile == 0) st_release_u64(st, lb_pack(LB_INC, epoch, tile_cnt));
-    else st_release_u64(st, lb_pack(LB_AGG, epoch, tile_cnt));
+    if (tile == 0) st_status_u64(st, lb_pack(LB_INC, epoch, tile_cnt));
+    else st_status_u64(st, lb_pack(LB_AGG, epoch, tile_cnt));
 
     uint32_t tot;
     const uint32_t local_start = block_excl_scan_256<uint32_t>(tile_cnt, s_scan, tot);
@@ -108,13 +106,13 @@ __global__ void __launch_bounds__(RS_THREADS, 2)
       const uint64_t ep = uint64_t(epoch & 0x3FFFFFu);
       int t = tile - 1;
       while (true) {
-        const uint64_t v = ld_acquire_u64(status + int64_t(t) * 256 + d);
+        const uint64_t v = ld_status_u64(status + int64_t(t) * 256 + d);
         if (((v >> 40) & 0x3FFFFFu) != ep || (v >> 62) == 0) continue;
         excl += v & ((1ull << 40) - 1);
         if ((v >> 62) == 2) break;
         --t;
       }
-      st_release_u64(st, lb_pack(LB_INC, epoch, excl + tile_cnt));
+      st_status_u64(st, lb_pack(LB_INC, epoch, excl + tile_cnt));
     }
     s_gbase[d] = digit_base[d] + int64_t(excl) - int64_t(local_start);
 #pragma unroll

@@ -6,32 +6,59 @@
 // neighbours (algorithms.py:108); total = sum over oriented arcs (u,v) of
 // |N+(u) ∩ N+(v)| (algorithms.py:110-116).
 //
-// Device pipeline:
-//   und_keys_kernel    out-CSR arcs -> (min,max) packed keys, self-loops -> sentinel
-//   radix_sort         2k bits
-//   und_dedupe_kernel  unique undirected pairs (m) + undirected degrees
-//   orient_kernel      pair -> arc from lower to higher (degree, id) rank
-//   radix_sort         2k bits
-//   segment<plain>     oriented CSR (off_p, adj_p), rows ascending by id
-//   tc_items_kernel    work items (u, block of 32 out-neighbours)
-//   tc_count_kernel    warp per item: N+(u) staged in shared memory; the
-//                      warp flattens the (v, w in N+(v)) pairs of its 32 v's
-//                      across lanes and binary-searches each w in N+(u)
-//                      (or N+(v) elements searched in N+(u) when shorter).
-// All counts are integers -> exact and order independent.
+// Device pipeline (everything after step 2 lives in RANK space: node r is the
+// r-th smallest (degree, id), so N+(r) ⊂ (r, n) and hubs sit at the top):
+//   1 cand_kernel<DEG>   edge-parallel over the 2E "candidate slots" out(i) ++
+//                        in(i): a slot is an undirected neighbour unless it is
+//                        a self-loop or an in-slot whose source is also in the
+//                        sorted out-row (binary search) -> undirected degree
+//   2 rank               radix sort of (degree, id) keys -> rank[id]
+//   3 cand_kernel<ARCS>  same slots; every candidate with a higher rank emits
+//                        the arc key rank(i)<<k | rank(j) (stream-compacted,
+//                        + digit histograms of its sort)
+//   4 radix sort + segment   -> oriented CSR N+ (rows and lists by rank)
+//   5 N- (transpose)     keys v<<32 | arc, stable sort on the v bits -> for
+//                        every v the arcs (u,v), in u order, as (first index
+//                        of N+(u) after v, remaining length): the "suffix"
+//   6 count              task = (v, chunk of N-(v)). The N+(v) membership
+//                        structure is a shared-memory BITMAP over (v, n) when
+//                        n-1-v <= TC_BM_BITS (the top ranks, where R-MAT puts
+//                        nearly all the work), else a hash table (per warp,
+//                        or per CTA for large d+(v)). For every arc (u,v) the
+//                        warp probes the suffix of N+(u) after v — exactly
+//                        the w > v candidates — flattened across 32 lanes so
+//                        reads stay coalesced; each triangle u<v<w is counted
+//                        once, at its middle vertex v.
+// Work = sum over u of d+(u)(d+(u)-1)/2 probes. All arithmetic is integer:
+// exact and independent of scheduling.
 #include "graph.cuh"
 #include "radix_sort.cuh"
 #include "scan.cuh"
 #include "segment.cuh"
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 namespace gtd {
 
-constexpr int TC_TILE = 2048;
-constexpr int TC_CAP = 1024;  // N+(u) staged in shared memory up to this size
+constexpr int TC_CAND_TILE = 2048;             // slots per CTA in cand_kernel
+constexpr int TC_ROWS_CAP = TC_CAND_TILE + 2;  // staged row offsets per tile
+constexpr int TC_SLOTS = 2048;                 // hash slots per warp (8 KB)
+constexpr int TC_WARP_MAX = TC_SLOTS / 4;      // largest d+(v) of a warp hash task
+constexpr int TC_CHUNK = 256;                  // arcs per warp task
+constexpr int TC_CHUNK_CTA = 1024;             // arcs per CTA task
+constexpr int TC_BM_BITS = 1 << 18;            // bitmap window (32 KB of shared memory)
+constexpr int32_t TC_EMPTY = -1;
 
-// Largest r in [lo, hi] with off[r] <= e (the row holding edge e).
+__global__ void __launch_bounds__(256) cat_off_kernel(const int64_t* __restrict__ out_off,
+                                                      const int64_t* __restrict__ in_off,
+                                                      int64_t n, int64_t* __restrict__ cat) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i <= n) cat[i] = out_off[i] + in_off[i];
+}
+
+// Largest r in [lo, hi] with off[r] <= e (the row holding slot e).
 __device__ __forceinline__ int64_t row_of(const int64_t* __restrict__ off, int64_t lo, int64_t hi,
                                           int64_t e) {
   while (lo < hi) {
@@ -42,214 +69,613 @@ __device__ __forceinline__ int64_t row_of(const int64_t* __restrict__ off, int64
   return lo;
 }
 
-__global__ void __launch_bounds__(256) und_keys_kernel(const int64_t* __restrict__ off,
-                                                       const int32_t* __restrict__ adj, int64_t n,
-                                                       int64_t e, int kbits, SortPlan plan,
-                                                       unsigned long long* __restrict__ hist,
-                                                       uint64_t* __restrict__ keys) {
-  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
-  __shared__ int64_t s_r[2];
-  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
-  const int64_t e0 = int64_t(blockIdx.x) * TC_TILE;
-  const int64_t e1 = min(e, e0 + TC_TILE);
-  if (threadIdx.x == 0) {
-    s_r[0] = row_of(off, 0, n - 1, e0);
-    s_r[1] = row_of(off, s_r[0], n - 1, e1 - 1);
-  }
-  __syncthreads();
-  constexpr int PER = TC_TILE / 256;
-  const int64_t my0 = e0 + int64_t(threadIdx.x) * PER;
-  if (my0 < e1) {
-    int64_t r = row_of(off, s_r[0], s_r[1], my0);
-    int64_t rend = off[r + 1];
-    for (int i = 0; i < PER; ++i) {
-      const int64_t ei = my0 + i;
-      if (ei >= e1) break;
-      while (ei >= rend) { ++r; rend = off[r + 1]; }
-      const uint64_t u = uint64_t(r), v = uint64_t(adj[ei]);
-      uint64_t key;
-      if (u == v) key = ~0ull;
-      else key = u < v ? ((u << kbits) | v) : ((v << kbits) | u);
-      keys[ei] = key;
-      plan_hist_add(sh, plan, key);
-    }
-  }
-  __syncthreads();
-  plan_hist_flush(sh, plan, hist);
-}
-
-// Unique undirected pairs (drop repeats and self-loop sentinels) + degrees.
-__global__ void __launch_bounds__(256) und_dedupe_kernel(const uint64_t* __restrict__ keys, int64_t n,
-                                                         int kbits, uint64_t* __restrict__ out,
-                                                         int32_t* __restrict__ deg,
-                                                         uint64_t* __restrict__ status,
-                                                         uint32_t* __restrict__ counter,
-                                                         uint32_t epoch,
-                                                         int64_t* __restrict__ total_out) {
-  __shared__ uint32_t s_warp[8];
-  __shared__ uint32_t s_tile;
-  __shared__ uint64_t s_excl;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_tile = atomicAdd(counter, 1u);
-  __syncthreads();
-  const int tile = int(s_tile);
-  const int64_t wbase = int64_t(tile) * SEG_TILE + int64_t(warp) * 32 * SEG_KPT;
-  const uint64_t mask2 = (kbits >= 32) ? ~0ull : ((1ull << (2 * kbits)) - 1ull);
-  uint64_t k[SEG_KPT];
-  uint32_t keep_bits = 0, before[SEG_KPT], run = 0;
-  const unsigned lt = lanemask_lt();
-#pragma unroll
-  for (int i = 0; i < SEG_KPT; ++i) {
-    const int64_t idx = wbase + i * 32 + lane;
-    k[i] = idx < n ? keys[idx] : ~0ull;
-    const bool keep = idx < n && (k[i] & mask2) != mask2 && (idx == 0 || keys[idx - 1] != k[i]);
-    keep_bits |= uint32_t(keep) << i;
-    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-    before[i] = run + __popc(bal & lt);
-    run += __popc(bal);
-  }
-  if (lane == 0) s_warp[warp] = run;
-  __syncthreads();
-  uint32_t wpre = 0, tcount = 0;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    const uint32_t c = s_warp[w];
-    if (w < warp) wpre += c;
-    tcount += c;
-  }
-  if (tid == 0) {
-    s_excl = lookback_single(status, tile, epoch, tcount);
-    if (int64_t(tile) == (n - 1) / SEG_TILE) *total_out = int64_t(s_excl) + tcount;
-  }
-  __syncthreads();
-  const int64_t base = int64_t(s_excl) + wpre;
-  const uint64_t low = (1ull << kbits) - 1ull;
-#pragma unroll
-  for (int i = 0; i < SEG_KPT; ++i) {
-    if ((keep_bits >> i) & 1u) {
-      out[base + before[i]] = k[i];
-      atomicAdd(&deg[k[i] >> kbits], 1);
-      atomicAdd(&deg[k[i] & low], 1);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256) orient_kernel(const uint64_t* __restrict__ pairs, int64_t m,
-                                                     int kbits, const int32_t* __restrict__ deg,
-                                                     SortPlan plan,
-                                                     unsigned long long* __restrict__ hist,
-                                                     uint64_t* __restrict__ arcs) {
-  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
-  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
-  __syncthreads();
-  const uint64_t low = (1ull << kbits) - 1ull;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
-    const uint64_t p = pairs[i];
-    const uint64_t a = p >> kbits, b = p & low;  // a < b by id
-    const int32_t da = deg[a], db = deg[b];
-    const bool a_low = da <= db;  // equal degree: the lower id (a) ranks lower
-    const uint64_t arc = a_low ? p : ((b << kbits) | a);
-    arcs[i] = arc;
-    plan_hist_add(sh, plan, arc);
-  }
-  __syncthreads();
-  plan_hist_flush(sh, plan, hist);
-}
-
-// Items: (u, first index of a block of 32 out-neighbours) for d+(u) >= 2.
-__global__ void __launch_bounds__(256) tc_item_count_kernel(const int64_t* __restrict__ off, int64_t n,
-                                                            int64_t* __restrict__ cnt) {
-  const int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (u >= n) return;
-  const int64_t d = off[u + 1] - off[u];
-  cnt[u] = d >= 2 ? (d + 31) / 32 : 0;
-}
-
-__global__ void __launch_bounds__(256) tc_item_fill_kernel(const int64_t* __restrict__ item_off,
-                                                           int64_t n, int2* __restrict__ items) {
-  const int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (u >= n) return;
-  const int64_t a = item_off[u], b = item_off[u + 1];
-  for (int64_t i = a; i < b; ++i) items[i] = make_int2(int(u), int(i - a));
-}
-
-__device__ __forceinline__ bool bsearch_in(const int32_t* list, int len, int32_t x) {
-  int lo = 0, hi = len;
+__device__ __forceinline__ bool bsearch_in(const int32_t* __restrict__ list, int64_t len,
+                                           int32_t x) {
+  int64_t lo = 0, hi = len;
   while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
+    const int64_t mid = (lo + hi) >> 1;
     if (list[mid] < x) lo = mid + 1;
     else hi = mid;
   }
   return lo < len && list[lo] == x;
 }
 
-__global__ void __launch_bounds__(256) tc_count_kernel(const int64_t* __restrict__ off,
-                                                       const int32_t* __restrict__ adj,
-                                                       const int2* __restrict__ items, int64_t n_items,
-                                                       unsigned int* __restrict__ next_item,
-                                                       unsigned long long* __restrict__ total) {
-  __shared__ int32_t s_list[8][TC_CAP];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned long long acc = 0;
-  int32_t* my = s_list[warp];
-  while (true) {
-    unsigned int it = 0;
-    if (lane == 0) it = atomicAdd(next_item, 1u);
-    it = __shfl_sync(0xffffffffu, it, 0);
-    if (int64_t(it) >= n_items) break;
-    const int2 item = items[it];
-    const int64_t u = item.x;
-    const int64_t ou = off[u];
-    const int du = int(off[u + 1] - ou);
-    const int32_t* lu;
-    if (du <= TC_CAP) {
-      for (int j = lane; j < du; j += 32) my[j] = adj[ou + j];
-      __syncwarp();
-      lu = my;
-    } else {
-      lu = adj + ou;
+enum CandMode { CAND_DEG = 0, CAND_ARCS = 1 };
+
+// Edge-parallel pass over the concatenated candidate slots of all rows.
+//   CAND_DEG:  deg[row] += candidate slots (undirected degree)
+//   CAND_ARCS: candidates j with rank[j] > rank[row] emit rank(row)<<k|rank(j),
+//              stream-compacted in slot order (decoupled look-back) + their
+//              radix digit histograms
+// The tile's row offsets are staged in shared memory (cat and out_off; the
+// in-offset is their difference), so the per-slot row search and offset
+// reads stay on chip; the per-slot global loads of all PER slots are issued
+// before any of them is consumed.
+template <int MODE>
+__global__ void __launch_bounds__(256) cand_kernel(
+    const int64_t* __restrict__ cat, const int64_t* __restrict__ out_off,
+    const int32_t* __restrict__ out_adj, const int32_t* __restrict__ in_adj, int64_t n,
+    int64_t slots, int32_t* __restrict__ deg, const int32_t* __restrict__ rank, int kbits,
+    SortPlan plan, unsigned long long* __restrict__ hist, uint64_t* __restrict__ arcs,
+    uint64_t* __restrict__ status, uint32_t* __restrict__ counter, uint32_t epoch,
+    int64_t* __restrict__ total_out) {
+  constexpr int PER = TC_CAND_TILE / 256;
+  __shared__ int64_t s_cat[TC_ROWS_CAP];
+  __shared__ int64_t s_oo[TC_ROWS_CAP];
+  __shared__ uint32_t sh[MODE == CAND_ARCS ? gt::RS_MAX_PASSES * 256 : 1];
+  __shared__ int64_t s_r[2];
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_warp[8];
+  __shared__ uint64_t s_excl;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (MODE == CAND_ARCS)
+    for (int i = tid; i < plan.passes * 256; i += 256) sh[i] = 0;
+  if (tid == 0) {
+    const uint32_t t = MODE == CAND_ARCS ? atomicAdd(counter, 1u) : blockIdx.x;
+    s_tile = t;
+    const int64_t e0 = int64_t(t) * TC_CAND_TILE;
+    const int64_t e1 = min(slots, e0 + TC_CAND_TILE) - 1;
+    s_r[0] = row_of(cat, 0, n - 1, e0);
+    s_r[1] = row_of(cat, s_r[0], n - 1, e1);
+  }
+  __syncthreads();
+  const int64_t e0 = int64_t(s_tile) * TC_CAND_TILE;
+  const int64_t r0 = s_r[0], r1 = s_r[1];
+  const int64_t nr = r1 - r0 + 2;  // rows r0..r1 plus the end offset of r1
+  const bool staged = nr <= TC_ROWS_CAP;
+  if (staged) {
+    for (int i = tid; i < int(nr); i += 256) {
+      s_cat[i] = cat[r0 + i];
+      s_oo[i] = out_off[r0 + i];
     }
-    // this item's 32 v's
-    const int j = item.y * 32 + lane;
-    int32_t v = -1;
-    int64_t ov = 0;
-    int dv = 0;
-    if (j < du) {
-      v = lu[j];
-      ov = off[v];
-      dv = int(off[v + 1] - ov);
-    }
-    const int incl = warp_incl_scan(dv);
-    const int tot = __shfl_sync(0xffffffffu, incl, 31);
-    const int excl = incl - dv;
-    unsigned int cnt = 0;
-    for (int t0 = 0; t0 < tot; t0 += 32) {
-      const int t = t0 + lane;
-      // owner lane: largest l with excl_l <= t
-      int lo = 0;
+  }
+  __syncthreads();
+  auto cat_at = [&](int64_t r) { return staged ? s_cat[r - r0] : cat[r]; };
+  auto oo_at = [&](int64_t r) { return staged ? s_oo[r - r0] : out_off[r]; };
+
+  // ---- per-slot values (no warp-collective operations: loads overlap) ----
+  int64_t row[PER];
+  int32_t j[PER];
+  bool cand[PER];
 #pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int cand = lo + step;
-        const int ex = __shfl_sync(0xffffffffu, excl, cand & 31);
-        if (cand < 32 && ex <= t) lo = cand;
+  for (int q = 0; q < PER; ++q) {
+    const int64_t e = e0 + int64_t(warp) * 32 * PER + q * 32 + lane;
+    row[q] = -1;
+    j[q] = 0;
+    cand[q] = false;
+    if (e < slots) {
+      int64_t lo = r0, hi = r1;  // largest r with cat(r) <= e
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (cat_at(mid) <= e) lo = mid;
+        else hi = mid - 1;
       }
-      const int64_t ovl = __shfl_sync(0xffffffffu, ov, lo);
-      const int exl = __shfl_sync(0xffffffffu, excl, lo);
-      if (t < tot) {
-        const int32_t w = adj[ovl + (t - exl)];
-        cnt += bsearch_in(lu, du, w) ? 1u : 0u;
+      const int64_t c = cat_at(lo), oa = oo_at(lo), no = oo_at(lo + 1) - oa;
+      const int64_t k = e - c;
+      row[q] = lo;
+      cand[q] = true;
+      j[q] = k < no ? out_adj[oa + k] : in_adj[(c - oa) + (k - no)];  // in_off = cat - out_off
+    }
+  }
+  // drop self-loops and in-slots whose source is also an out-neighbour
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    if (!cand[q]) continue;
+    const int64_t r = row[q];
+    cand[q] = j[q] != int32_t(r);
+    const int64_t e = e0 + int64_t(warp) * 32 * PER + q * 32 + lane;
+    const int64_t oa = oo_at(r), no = oo_at(r + 1) - oa;
+    if (cand[q] && e - cat_at(r) >= no) cand[q] = !bsearch_in(out_adj + oa, no, j[q]);
+  }
+
+  if (MODE == CAND_DEG) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const bool valid = row[q] >= 0;
+      const unsigned active = __ballot_sync(0xffffffffu, valid);
+      const unsigned kb = __ballot_sync(0xffffffffu, cand[q]);
+      if (valid) {
+        const unsigned peers = __match_any_sync(active, (unsigned long long)row[q]);
+        const int c = __popc(kb & peers);
+        if (lane == __ffs(peers) - 1 && c) atomicAdd(&deg[row[q]], c);
       }
     }
-    acc += warp_sum(cnt);
+    return;
+  }
+
+  // ---- CAND_ARCS: rank-space arc keys, compaction ranks -------------------
+  uint64_t key[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    key[q] = 0;
+    if (cand[q]) {
+      const int32_t ri = rank[row[q]], rj = rank[j[q]];
+      cand[q] = rj > ri;
+      key[q] = (uint64_t(ri) << kbits) | uint64_t(rj);
+    }
+  }
+  const unsigned lt = lanemask_lt();
+  uint32_t before[PER], run = 0, bits = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const unsigned b = __ballot_sync(0xffffffffu, cand[q]);
+    bits |= uint32_t(cand[q]) << q;
+    before[q] = run + __popc(b & lt);
+    run += __popc(b);
+    if (cand[q]) plan_hist_add(sh, plan, key[q]);
+  }
+  if (lane == 0) s_warp[warp] = run;
+  __syncthreads();
+  uint32_t pre = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    const uint32_t a = s_warp[w];
+    if (w < warp) pre += a;
+    tot += a;
+  }
+  if (tid == 0) {
+    s_excl = lookback_single(status, int(s_tile), epoch, tot);
+    if (int64_t(s_tile) == (slots - 1) / TC_CAND_TILE) *total_out = int64_t(s_excl) + tot;
+  }
+  __syncthreads();
+  const int64_t base = int64_t(s_excl) + pre;
+#pragma unroll
+  for (int q = 0; q < PER; ++q)
+    if ((bits >> q) & 1u) arcs[base + before[q]] = key[q];
+  plan_hist_flush(sh, plan, hist);
+}
+
+// ---- rank (algorithms.py:103-106: lexsort by (degree, id)) ------------------
+
+__global__ void __launch_bounds__(256) rank_keys_kernel(const int32_t* __restrict__ deg, int64_t n,
+                                                        int kbits, SortPlan plan,
+                                                        unsigned long long* __restrict__ hist,
+                                                        uint64_t* __restrict__ keys) {
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
+  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t k = (uint64_t(uint32_t(deg[i])) << kbits) | uint64_t(i);
+    keys[i] = k;
+    plan_hist_add(sh, plan, k);
+  }
+  __syncthreads();
+  plan_hist_flush(sh, plan, hist);
+}
+
+__global__ void __launch_bounds__(256) rank_scatter_kernel(const uint64_t* __restrict__ sorted,
+                                                           int64_t n, uint64_t lowmask,
+                                                           int32_t* __restrict__ rank) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r < n) rank[sorted[r] & lowmask] = int32_t(r);
+}
+
+__global__ void __launch_bounds__(256) max_i32_kernel(const int32_t* __restrict__ x, int64_t n,
+                                                      int* __restrict__ out) {
+  int mx = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    mx = max(mx, x[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
+}
+
+// ---- N-: the transpose of N+ with arc positions ----------------------------
+
+__global__ void __launch_bounds__(256) nminus_keys_kernel(const int32_t* __restrict__ adj_p,
+                                                          int64_t m, SortPlan plan,
+                                                          unsigned long long* __restrict__ hist,
+                                                          uint64_t* __restrict__ keys) {
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
+  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t a = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; a < m; a += stride) {
+    const uint64_t k = (uint64_t(uint32_t(adj_p[a])) << 32) | uint64_t(a);
+    keys[a] = k;
+    plan_hist_add(sh, plan, k);
+  }
+  __syncthreads();
+  plan_hist_flush(sh, plan, hist);
+}
+
+// Remaining length of N+(u) after each arc: warp per row.
+__global__ void __launch_bounds__(256) suffix_len_kernel(const int64_t* __restrict__ off_p,
+                                                         int64_t n, int32_t* __restrict__ sl) {
+  const int64_t wg = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t u = wg; u < n; u += nw) {
+    const int64_t a = off_p[u], b = off_p[u + 1];
+    for (int64_t k = a + lane; k < b; k += 32) sl[k] = int32_t(b - k - 1);
+  }
+}
+
+// N-(v) entries -> (first position after v in N+(u), remaining length).
+__global__ void __launch_bounds__(256) nminus_fill_kernel(const int32_t* __restrict__ arc_of,
+                                                          const int32_t* __restrict__ sl, int64_t m,
+                                                          int2* __restrict__ nm) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const int32_t a = arc_of[i];
+    nm[i] = make_int2(a + 1, sl[a]);
+  }
+}
+
+// ---- work lists --------------------------------------------------------------
+// kind 0: bitmap CTA tasks (n-1-v <= TC_BM_BITS), 1: warp hash tasks,
+// 2: CTA hash tasks. A task is (v, chunk of N-(v)); it needs d+(v), d-(v) >= 1.
+__global__ void __launch_bounds__(256) tc_task_count_kernel(const int64_t* __restrict__ off_p,
+                                                            const int64_t* __restrict__ off_m,
+                                                            int64_t n, int64_t* __restrict__ c0,
+                                                            int64_t* __restrict__ c1,
+                                                            int64_t* __restrict__ c2) {
+  const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int64_t dp = off_p[v + 1] - off_p[v];
+  const int64_t dm = off_m[v + 1] - off_m[v];
+  const bool live = dp >= 1 && dm >= 1;
+  const bool bm = n - 1 - v <= TC_BM_BITS;
+  c0[v] = (live && bm) ? (dm + TC_CHUNK_CTA - 1) / TC_CHUNK_CTA : 0;
+  c1[v] = (live && !bm && dp <= TC_WARP_MAX) ? (dm + TC_CHUNK - 1) / TC_CHUNK : 0;
+  c2[v] = (live && !bm && dp > TC_WARP_MAX) ? (dm + TC_CHUNK_CTA - 1) / TC_CHUNK_CTA : 0;
+}
+
+__global__ void __launch_bounds__(256) tc_task_fill_kernel(const int64_t* __restrict__ toff,
+                                                           int64_t n, int2* __restrict__ tasks) {
+  const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int64_t a = toff[v], b = toff[v + 1];
+  for (int64_t i = a; i < b; ++i) tasks[i] = make_int2(int(v), int(i - a));
+}
+
+__global__ void __launch_bounds__(256) max_dplus_kernel(const int64_t* __restrict__ off, int64_t n,
+                                                        unsigned long long* __restrict__ out) {
+  unsigned long long mx = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < n; u += stride)
+    mx = max(mx, (unsigned long long)(off[u + 1] - off[u]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
+}
+
+// ---- membership structures of N+(v) ------------------------------------------
+
+__device__ __forceinline__ uint32_t tc_hash(int32_t x, int log_slots) {
+  return (uint32_t(x) * 0x9E3779B1u) >> (32 - log_slots);
+}
+
+struct HashProbe {
+  int32_t* tab;
+  uint32_t mask;
+  int log_slots;
+  __device__ __forceinline__ void insert(int32_t x) const {
+    uint32_t h = tc_hash(x, log_slots);
+    while (atomicCAS(&tab[h], TC_EMPTY, x) != TC_EMPTY) h = (h + 1) & mask;
+  }
+  __device__ __forceinline__ bool operator()(int32_t x) const {
+    uint32_t h = tc_hash(x, log_slots);
+    while (true) {
+      const int32_t y = tab[h];
+      if (y == x) return true;
+      if (y == TC_EMPTY) return false;
+      h = (h + 1) & mask;
+    }
+  }
+};
+
+// Bit (w - v - 1) of the window (v, v + 1 + bits) for every w in N+(v).
+struct BitmapProbe {
+  const uint32_t* bm;
+  int32_t base;  // v + 1
+  __device__ __forceinline__ bool operator()(int32_t w) const {
+    const uint32_t i = uint32_t(w - base);
+    return (bm[i >> 5] >> (i & 31)) & 1u;
+  }
+};
+
+__device__ __forceinline__ int tc_log_slots(int64_t d, int cap_log) {
+  int l = 5;  // >= 32 slots, >= 4 slots per element (load <= 1/4)
+  while (l < cap_log && (int64_t(1) << l) < 4 * d) ++l;
+  return l;
+}
+
+// One warp probes up to 32 suffixes (lane = arc (u,v): positions [s, s+len)
+// of adj, all w > v) against N+(v): position t of the concatenation of the 32
+// suffixes belongs to the lane whose suffix starts last at or before t, so
+// consecutive lanes read consecutive elements (coalesced) whatever the
+// lengths. TC_WIN windows of 32 positions are resolved per step and their
+// loads issued together (TC_WIN independent reads in flight per lane).
+constexpr int TC_WIN = 4;
+
+template <typename Probe>
+__device__ __forceinline__ uint32_t tc_wedges32(const int32_t* __restrict__ adj, int2 suffix,
+                                                const Probe& probe,
+                                                uint8_t* s_start /* [32 * TC_WIN] */) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ou = suffix.x;
+  const int du = suffix.y;
+  const int incl = warp_incl_scan(du);
+  const int tot = __shfl_sync(0xffffffffu, incl, 31);
+  const int excl = incl - du;
+  uint32_t cnt = 0;
+  int carry = 0;
+  for (int t0 = 0; t0 < tot; t0 += 32 * TC_WIN) {
+    // suffixes starting in this step: position -> lane map + per-window masks
+    const int rel = excl - t0;
+    const bool st = du > 0 && rel >= 0 && rel < 32 * TC_WIN;
+    if (st) s_start[rel] = uint8_t(lane);
+    unsigned starts[TC_WIN];
+#pragma unroll
+    for (int q = 0; q < TC_WIN; ++q)
+      starts[q] = __reduce_or_sync(0xffffffffu, (st && (rel >> 5) == q) ? 1u << (rel & 31) : 0u);
+    __syncwarp();
+    int32_t w[TC_WIN];
+#pragma unroll
+    for (int q = 0; q < TC_WIN; ++q) {
+      const unsigned mine = starts[q] & (0xffffffffu >> (31 - lane));
+      const int owner = mine ? int(s_start[32 * q + 31 - __clz(mine)]) : carry;
+      carry = __shfl_sync(0xffffffffu, owner, 31);
+      const int64_t o = __shfl_sync(0xffffffffu, ou, owner);
+      const int ex = __shfl_sync(0xffffffffu, excl, owner);
+      const int t = t0 + 32 * q + lane;
+      w[q] = t < tot ? __ldg(adj + o + (t - ex)) : TC_EMPTY;
+    }
+#pragma unroll
+    for (int q = 0; q < TC_WIN; ++q)
+      if (w[q] != TC_EMPTY) cnt += probe(w[q]) ? 1u : 0u;
     __syncwarp();
   }
+  return cnt;
+}
+
+// Bitmap tasks: CTA per (v, chunk of N-(v)), bitmap of (v, n) in shared memory.
+__global__ void __launch_bounds__(256) tc_count_bitmap_kernel(
+    const int64_t* __restrict__ off_p, const int32_t* __restrict__ adj_p,
+    const int64_t* __restrict__ off_m, const int2* __restrict__ nm,
+    const int2* __restrict__ tasks, int64_t n_tasks, int64_t n,
+    unsigned long long* __restrict__ total) {
+  extern __shared__ uint32_t s_bm[];  // TC_BM_BITS / 32 words
+  __shared__ uint8_t s_start[8][32 * TC_WIN];
+  __shared__ unsigned long long s_red[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long acc = 0;
+  for (int64_t it = blockIdx.x; it < n_tasks; it += gridDim.x) {
+    const int2 task = tasks[it];
+    const int v = task.x;
+    const int64_t ov = off_p[v];
+    const int dv = int(off_p[v + 1] - ov);
+    const int nwords = int((n - 1 - v + 31) >> 5);
+    __syncthreads();  // previous task done with the bitmap
+    for (int i = threadIdx.x; i < nwords; i += 256) s_bm[i] = 0u;
+    __syncthreads();
+    for (int i = threadIdx.x; i < dv; i += 256) {
+      const uint32_t b = uint32_t(adj_p[ov + i] - v - 1);
+      atomicOr(&s_bm[b >> 5], 1u << (b & 31));
+    }
+    __syncthreads();
+    const BitmapProbe probe{s_bm, v + 1};
+    const int64_t om = off_m[v];
+    const int dm = int(off_m[v + 1] - om);
+    const int begin = task.y * TC_CHUNK_CTA;
+    const int end = min(dm, begin + TC_CHUNK_CTA);
+    uint32_t cnt = 0;
+    for (int jb = begin + warp * 32; jb < end; jb += 256) {
+      const int jj = jb + lane;
+      const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
+      cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
+    }
+    acc += cnt;
+  }
+  acc = block_sum_256(acc, s_red);
+  if (threadIdx.x == 0 && acc) atomicAdd(total, acc);
+}
+
+// Hash tasks, warp per (v, chunk): N+(v) in a per-warp table (load <= 1/4).
+__global__ void __launch_bounds__(256) tc_count_warp_kernel(
+    const int64_t* __restrict__ off_p, const int32_t* __restrict__ adj_p,
+    const int64_t* __restrict__ off_m, const int2* __restrict__ nm,
+    const int2* __restrict__ tasks, int64_t n_tasks, unsigned int* __restrict__ next_task,
+    unsigned long long* __restrict__ total) {
+  extern __shared__ int32_t s_tab[];  // [8][TC_SLOTS]
+  __shared__ uint8_t s_start[8][32 * TC_WIN];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* tab = s_tab + warp * TC_SLOTS;
+  int cur_v = -1;
+  HashProbe probe{tab, 31u, 5};
+  unsigned long long acc = 0;
+  while (true) {
+    unsigned int it = 0;
+    if (lane == 0) it = atomicAdd(next_task, 1u);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (int64_t(it) >= n_tasks) break;
+    const int2 task = tasks[it];
+    const int v = task.x;
+    if (v != cur_v) {
+      const int64_t ov = off_p[v];
+      const int dv = int(off_p[v + 1] - ov);
+      probe.log_slots = tc_log_slots(dv, 11);
+      probe.mask = (1u << probe.log_slots) - 1u;
+      for (int i = lane; i <= int(probe.mask); i += 32) tab[i] = TC_EMPTY;
+      __syncwarp();
+      for (int i = lane; i < dv; i += 32) probe.insert(adj_p[ov + i]);
+      __syncwarp();
+      cur_v = v;
+    }
+    const int64_t om = off_m[v];
+    const int dm = int(off_m[v + 1] - om);
+    const int end = min(dm, (task.y + 1) * TC_CHUNK);
+    uint32_t cnt = 0;
+    for (int jb = task.y * TC_CHUNK; jb < end; jb += 32) {
+      const int jj = jb + lane;
+      const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
+      cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
+    }
+    acc += cnt;
+  }
+  acc = warp_sum(acc);
   if (lane == 0 && acc) atomicAdd(total, acc);
+}
+
+// Hash tasks with large d+(v), CTA per (v, chunk); table in dynamic shared
+// memory, or in `gtab` (2^log_slots per CTA) when it does not fit.
+__global__ void __launch_bounds__(256) tc_count_cta_kernel(
+    const int64_t* __restrict__ off_p, const int32_t* __restrict__ adj_p,
+    const int64_t* __restrict__ off_m, const int2* __restrict__ nm,
+    const int2* __restrict__ tasks, int64_t n_tasks, int log_slots, int32_t* __restrict__ gtab,
+    unsigned long long* __restrict__ total) {
+  extern __shared__ int32_t s_dyn[];
+  __shared__ uint8_t s_start[8][32 * TC_WIN];
+  __shared__ unsigned long long s_red[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* tab = gtab ? gtab + (int64_t(blockIdx.x) << log_slots) : s_dyn;
+  const HashProbe probe{tab, (1u << log_slots) - 1u, log_slots};
+  unsigned long long acc = 0;
+  for (int64_t it = blockIdx.x; it < n_tasks; it += gridDim.x) {
+    const int2 task = tasks[it];
+    const int v = task.x;
+    const int64_t ov = off_p[v];
+    const int dv = int(off_p[v + 1] - ov);
+    __syncthreads();  // previous task done with the table
+    for (int i = threadIdx.x; i <= int(probe.mask); i += 256) tab[i] = TC_EMPTY;
+    __syncthreads();
+    for (int i = threadIdx.x; i < dv; i += 256) probe.insert(adj_p[ov + i]);
+    __syncthreads();
+    const int64_t om = off_m[v];
+    const int dm = int(off_m[v + 1] - om);
+    const int begin = task.y * TC_CHUNK_CTA;
+    const int end = min(dm, begin + TC_CHUNK_CTA);
+    uint32_t cnt = 0;
+    for (int jb = begin + warp * 32; jb < end; jb += 256) {
+      const int jj = jb + lane;
+      const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
+      cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
+    }
+    acc += cnt;
+  }
+  acc = block_sum_256(acc, s_red);
+  if (threadIdx.x == 0 && acc) atomicAdd(total, acc);
 }
 
 }  // namespace gtd
 
 namespace gt {
+
+static int grid_cap(int64_t blocks) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, 8LL * ctx().sm_count)));
+}
+
+// Degree-ordered orientation in rank space (device scratch, valid until the
+// next library call that uses the workspace).
+struct Oriented {
+  int64_t n = 0, m = 0;
+  int kbits = 1;
+  int32_t* deg = nullptr;    // [n] by id
+  int32_t* rank = nullptr;   // [n] id -> rank
+  int64_t* off_p = nullptr;  // [n+1] by rank
+  int32_t* adj_p = nullptr;  // [m] ranks, ascending per row
+};
+
+static Oriented orient(const gt_graph* g) {
+  const int64_t n = g->n, e = g->e;
+  cudaStream_t s = ctx().stream;
+  int64_t* small = ws_n<int64_t>(WS_SMALL, 16);
+  uint32_t* counters = ws_n<uint32_t>(WS_COUNTERS, 64);
+  const int64_t slots = 2 * e;
+  Oriented o;
+  o.n = n;
+  o.kbits = bits_for(n);
+  // scratch: cat | off_p (n+1 each) | deg[n] | rank[n]
+  const size_t need = size_t(n + 1) * 8 * 2 + size_t(n) * 8 + 64;
+  char* p = static_cast<char*>(ws_get(WS_TMP3, need));
+  int64_t* cat = reinterpret_cast<int64_t*>(p);
+  o.off_p = cat + (n + 1);
+  o.deg = reinterpret_cast<int32_t*>(o.off_p + (n + 1));
+  o.rank = o.deg + n;
+  o.adj_p = ws_n<int32_t>(WS_TMP2, size_t(e) + 1);  // m <= E
+
+  const int64_t tiles = ceil_div64(slots, gtd::TC_CAND_TILE);
+  if (tiles >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangles: too many slot tiles");
+  const double cand_bytes = 8.0 * (n + 1) * 3 + 4.0 * slots + 4.0 * n;
+  // 1. undirected degrees over the concatenated (out ++ in) rows
+  GT_CUDA(cudaMemsetAsync(o.deg, 0, size_t(n) * 4, s));
+  GT_CUDA(cudaMemsetAsync(small + 12, 0, 8, s));
+  {
+    Phase ph("tc.und_degree", cand_bytes);
+    GT_LAUNCH(gtd::cat_off_kernel, ceil_div(n + 1, 256), 256, 0, g->out_off, g->in_off, n, cat);
+    GT_LAUNCH(gtd::cand_kernel<gtd::CAND_DEG>, static_cast<int>(tiles), 256, 0, cat, g->out_off,
+              g->out_adj, g->in_adj, n, slots, o.deg, (const int32_t*)nullptr, 0, SortPlan(),
+              (unsigned long long*)nullptr, (uint64_t*)nullptr, (uint64_t*)nullptr,
+              (uint32_t*)nullptr, 0u, (int64_t*)nullptr);
+    GT_LAUNCH(gtd::max_i32_kernel, grid_cap(ceil_div64(n, 256)), 256, 0, o.deg, n,
+              reinterpret_cast<int*>(small + 12));
+  }
+  int max_deg = 0;
+  d2h(&max_deg, small + 12, 4);
+  sync();
+  uint64_t* ka = ws_n<uint64_t>(WS_KEYS_A, size_t(std::max(n, e)));
+  uint64_t* kbuf = ws_n<uint64_t>(WS_KEYS_B, size_t(std::max(n, e)));
+  // 2. rank = position in (degree, id) order
+  {
+    SortPlan plan = make_plan(0, o.kbits + bits_for(int64_t(max_deg) + 1));
+    SortHist h = sort_hist_begin(0);
+    {
+      Phase ph("tc.rank", 12.0 * n);
+      GT_LAUNCH(gtd::rank_keys_kernel, grid_cap(ceil_div64(n, 1024)), 256, 0, o.deg, n, o.kbits,
+                plan, h.hist, ka);
+    }
+    uint64_t* sorted = radix_sort(ka, kbuf, n, plan, h, "tc.sort");
+    Phase ph("tc.rank", 12.0 * n);
+    GT_LAUNCH(gtd::rank_scatter_kernel, ceil_div(n, 256), 256, 0, sorted, n,
+              (uint64_t(1) << o.kbits) - 1, o.rank);
+  }
+  // 3. arcs to higher ranks, as rank-space keys
+  SortPlan aplan = make_plan(0, 2 * o.kbits);
+  SortHist ah = sort_hist_begin(0);
+  {
+    Phase ph("tc.orient", cand_bytes + 8.0 * slots);
+    uint64_t* status = ws_n<uint64_t>(WS_LOOKBACK, size_t(tiles) + 1);
+    GT_CUDA(cudaMemsetAsync(counters + 20, 0, 4, s));
+    GT_LAUNCH(gtd::cand_kernel<gtd::CAND_ARCS>, static_cast<int>(tiles), 256, 0, cat,
+              g->out_off, g->out_adj, g->in_adj, n, slots, o.deg, o.rank, o.kbits, aplan,
+              ah.hist, ka, status, counters + 20, next_epoch(), small + 4);
+  }
+  d2h(&o.m, small + 4, 8);
+  sync();
+  profile_add_bytes("tc.orient", 8.0 * o.m);
+  // 4. oriented CSR in rank space
+  uint64_t* arcs = radix_sort(ka, kbuf, o.m, aplan, ah, "tc.sort");
+  {
+    Phase ph("tc.oriented_csr", 12.0 * o.m + 8.0 * n);
+    if (o.m > 0)
+      GT_LAUNCH(gtd::segment_kernel<false>, ceil_div(o.m, gtd::SEG_TILE), 256, 0, arcs, o.m,
+                o.kbits, n, o.adj_p, o.off_p, (uint64_t*)nullptr, SortPlan(),
+                (unsigned long long*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr, 0u,
+                (int64_t*)nullptr);
+    else
+      GT_CUDA(cudaMemsetAsync(o.off_p, 0, size_t(n + 1) * 8, s));
+  }
+  return o;
+}
+
+void triangle_orientation(const gt_graph* g, int32_t* h_deg, int32_t* h_rank, int64_t* h_off_p,
+                          int32_t* h_adj_p, int64_t* m_out) {
+  require_init();
+  if (!g) fail(GT_EINVAL, "null graph");
+  *m_out = 0;
+  if (g->n == 0) return;
+  if (g->e == 0) fail(GT_EINVAL, "graph has no edges");
+  Oriented o = orient(g);
+  *m_out = o.m;
+  if (h_deg) d2h(h_deg, o.deg, size_t(g->n) * 4);
+  if (h_rank) d2h(h_rank, o.rank, size_t(g->n) * 4);
+  if (h_off_p) d2h(h_off_p, o.off_p, size_t(g->n + 1) * 8);
+  if (h_adj_p) d2h(h_adj_p, o.adj_p, size_t(o.m) * 4);
+  sync();
+}
 
 int64_t triangles(const gt_graph* g) {
   require_init();
@@ -257,84 +683,112 @@ int64_t triangles(const gt_graph* g) {
   const int64_t n = g->n, e = g->e;
   if (n == 0 || e == 0) return 0;
   cudaStream_t s = ctx().stream;
-  const int kb = g->kbits;
   int64_t* small = ws_n<int64_t>(WS_SMALL, 16);
   uint32_t* counters = ws_n<uint32_t>(WS_COUNTERS, 64);
-  uint64_t* ka = ws_n<uint64_t>(WS_KEYS_A, size_t(e));
-  uint64_t* kbuf = ws_n<uint64_t>(WS_KEYS_B, size_t(e));
-
-  // 1. undirected pair keys from the out-CSR
-  SortPlan plan = make_plan(0, 2 * kb);
-  SortHist h0 = sort_hist_begin(0);
-  {
-    Phase ph("tc.und_keys", 4.0 * e + 8.0 * n + 8.0 * e);
-    GT_LAUNCH(gtd::und_keys_kernel, ceil_div(e, gtd::TC_TILE), 256, 0, g->out_off, g->out_adj, n, e,
-              kb, plan, h0.hist, ka);
-  }
-  uint64_t* sorted = radix_sort(ka, kbuf, e, plan, h0, "tc.sort");
-  uint64_t* other = sorted == ka ? kbuf : ka;
-
-  // 2. unique undirected pairs + degrees
-  int32_t* deg = ws_n<int32_t>(WS_TMP2, size_t(n));
-  GT_CUDA(cudaMemsetAsync(deg, 0, size_t(n) * 4, s));
-  {
-    Phase ph("tc.und_dedupe", 8.0 * e);
-    const int64_t tiles = ceil_div64(e, gtd::SEG_TILE);
-    uint64_t* status = ws_n<uint64_t>(WS_LOOKBACK, size_t(tiles) * 256);
-    GT_CUDA(cudaMemsetAsync(counters + 20, 0, 4, s));
-    GT_LAUNCH(gtd::und_dedupe_kernel, static_cast<int>(tiles), 256, 0, sorted, e, kb, other, deg,
-              status, counters + 20, next_epoch(), small + 4);
-  }
-  int64_t m = 0;
-  d2h(&m, small + 4, 8);
-  sync();
-  profile_add_bytes("tc.und_dedupe", 8.0 * m + 8.0 * m);
+  const Oriented o = orient(g);
+  const int64_t m = o.m;
   if (m == 0) return 0;
+  if (m >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangles: >= 2^31 undirected edges");
 
-  // 3. orient by (degree, id) and sort arcs
-  SortHist h1 = sort_hist_begin(1);
+  // 5. N-: arcs (u,v) grouped by v (stable: u ascending), as suffixes of N+(u)
+  char* p = static_cast<char*>(ws_get(WS_TMP1, size_t(m) * 8 + size_t(m) * 4 * 2 +
+                                                    size_t(n + 1) * 8 * 4 + 256));
+  auto carve = [&](size_t b) { char* r = p; p += (b + 15) & ~size_t(15); return r; };
+  int2* nm = reinterpret_cast<int2*>(carve(size_t(m) * 8));
+  int32_t* arc_of = reinterpret_cast<int32_t*>(carve(size_t(m) * 4));
+  int32_t* sl = reinterpret_cast<int32_t*>(carve(size_t(m) * 4));
+  int64_t* off_m = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
+  int64_t* t0 = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
+  int64_t* t1 = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
+  int64_t* t2 = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
+  uint64_t* ka = ws_n<uint64_t>(WS_KEYS_A, size_t(m));
+  uint64_t* kbuf = ws_n<uint64_t>(WS_KEYS_B, size_t(m));
   {
-    Phase ph("tc.orient", 16.0 * m);
-    const int grid = static_cast<int>(std::min<int64_t>(ceil_div64(m, 1024), 8LL * ctx().sm_count));
-    GT_LAUNCH(gtd::orient_kernel, grid, 256, 0, other, m, kb, deg, plan, h1.hist, sorted);
-  }
-  uint64_t* arcs = radix_sort(sorted, other, m, plan, h1, "tc.sort");
-
-  // 4. oriented CSR
-  const size_t need = size_t(n + 1) * 8 * 2 + size_t(m) * 4 + 64;
-  char* p = static_cast<char*>(ws_get(WS_TMP3, need));
-  int64_t* off_p = reinterpret_cast<int64_t*>(p);
-  int64_t* item_off = off_p + (n + 1);
-  int32_t* adj_p = reinterpret_cast<int32_t*>(item_off + (n + 1));
-  {
-    Phase ph("tc.oriented_csr", 12.0 * m + 8.0 * n);
-    GT_LAUNCH(gtd::segment_kernel<false>, ceil_div(m, gtd::SEG_TILE), 256, 0, arcs, m, kb, n, adj_p,
-              off_p, (uint64_t*)nullptr, SortPlan(), (unsigned long long*)nullptr,
+    SortPlan plan = make_plan(32, 32 + o.kbits);
+    SortHist h = sort_hist_begin(1);
+    {
+      Phase ph("tc.nminus", 12.0 * m);
+      GT_LAUNCH(gtd::nminus_keys_kernel, grid_cap(ceil_div64(m, 1024)), 256, 0, o.adj_p, m, plan,
+                h.hist, ka);
+    }
+    uint64_t* sorted = radix_sort(ka, kbuf, m, plan, h, "tc.sort");
+    Phase ph("tc.nminus", 12.0 * m + 8.0 * n + 4.0 * m + 8.0 * (n + 1) + 4.0 * m + 12.0 * m);
+    GT_LAUNCH(gtd::segment_kernel<false>, ceil_div(m, gtd::SEG_TILE), 256, 0, sorted, m, 32, n,
+              arc_of, off_m, (uint64_t*)nullptr, SortPlan(), (unsigned long long*)nullptr,
               (uint64_t*)nullptr, (uint32_t*)nullptr, 0u, (int64_t*)nullptr);
+    GT_LAUNCH(gtd::suffix_len_kernel, grid_cap(ceil_div64(n, 8)), 256, 0, o.off_p, n, sl);
+    GT_LAUNCH(gtd::nminus_fill_kernel, grid_cap(ceil_div64(m, 1024)), 256, 0, arc_of, sl, m, nm);
   }
-
-  // 5. work items: (u, block of 32 out-neighbours) for every u with d+(u) >= 2
-  int64_t n_items = 0;
+  // 6. work lists
   {
-    Phase ph("tc.items", 16.0 * n);
-    GT_LAUNCH(gtd::tc_item_count_kernel, ceil_div(n, 256), 256, 0, off_p, n, item_off);
-    exclusive_scan_i64(item_off, n, small + 5);
+    Phase ph("tc.tasks", 8.0 * (n + 1) * 8);
+    GT_CUDA(cudaMemsetAsync(small + 7, 0, 8, s));
+    GT_LAUNCH(gtd::tc_task_count_kernel, ceil_div(n, 256), 256, 0, o.off_p, off_m, n, t0, t1, t2);
+    exclusive_scan_i64(t0, n, small + 8);
+    exclusive_scan_i64(t1, n, small + 9);
+    exclusive_scan_i64(t2, n, small + 10);
+    GT_LAUNCH(gtd::max_dplus_kernel, grid_cap(ceil_div64(n, 256)), 256, 0, o.off_p, n,
+              reinterpret_cast<unsigned long long*>(small + 7));
   }
-  d2h(&n_items, small + 5, 8);
+  int64_t h[4];
+  d2h(h, small + 7, sizeof h);  // max d+, bitmap / warp / CTA task counts
   sync();
+  const int64_t max_dp = h[0], n_bm = h[1], n_wt = h[2], n_ct = h[3];
+  if (n_bm + n_wt + n_ct >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangle work list too long");
+  int2* tasks = ws_n<int2>(WS_TMP0, size_t(n_bm + n_wt + n_ct) + 1);
+  {
+    Phase ph("tc.tasks", 8.0 * (n_bm + n_wt + n_ct));
+    if (n_bm) GT_LAUNCH(gtd::tc_task_fill_kernel, ceil_div(n, 256), 256, 0, t0, n, tasks);
+    if (n_wt) GT_LAUNCH(gtd::tc_task_fill_kernel, ceil_div(n, 256), 256, 0, t1, n, tasks + n_bm);
+    if (n_ct)
+      GT_LAUNCH(gtd::tc_task_fill_kernel, ceil_div(n, 256), 256, 0, t2, n, tasks + n_bm + n_wt);
+  }
   unsigned long long* total = reinterpret_cast<unsigned long long*>(small + 6);
   GT_CUDA(cudaMemsetAsync(total, 0, 8, s));
-  if (n_items > 0) {
-    if (n_items >= (int64_t(1) << 32)) fail(GT_ECAPACITY, "triangle work list too long");
-    int2* items = ws_n<int2>(WS_TMP0, size_t(n_items));
-    GT_CUDA(cudaMemsetAsync(counters + 21, 0, 4, s));
-    {
-      Phase ph("tc.items", 8.0 * n_items);
-      GT_LAUNCH(gtd::tc_item_fill_kernel, ceil_div(n, 256), 256, 0, item_off, n, items);
+  // algorithmic bytes credited: every N- entry and N+ list once (the probed
+  // suffix elements depend on the graph and are not counted)
+  if (n_bm) {
+    Phase ph("tc.count", 8.0 * m + 4.0 * m);
+    const int words = int((std::min<int64_t>(n, gtd::TC_BM_BITS) + 31) / 32);
+    const int smem = words * 4;
+    if (smem > 48 * 1024)
+      GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_bitmap_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int grid = static_cast<int>(std::min<int64_t>(n_bm, 6LL * ctx().sm_count));
+    GT_LAUNCH(gtd::tc_count_bitmap_kernel, grid, 256, smem, o.off_p, o.adj_p, off_m, nm, tasks,
+              n_bm, n, total);
+  }
+  if (n_wt) {
+    Phase ph("tc.count_hash", 0.0);
+    GT_CUDA(cudaMemsetAsync(counters + 22, 0, 4, s));
+    const int smem = 8 * gtd::TC_SLOTS * 4;
+    GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_warp_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    GT_LAUNCH(gtd::tc_count_warp_kernel, ctx().sm_count * 3, 256, smem, o.off_p, o.adj_p, off_m,
+              nm, tasks + n_bm, n_wt, counters + 22, total);
+  }
+  if (n_ct) {
+    Phase ph("tc.count_hash", 0.0);
+    int log_slots = 5;
+    while ((int64_t(1) << log_slots) < 4 * max_dp) ++log_slots;
+    const size_t tab_bytes = size_t(4) << log_slots;
+    const int grid = static_cast<int>(std::min<int64_t>(n_ct, 2LL * ctx().sm_count));
+    // GT_TC_TABLE_SMEM_MAX (bytes) lowers the shared-memory cap (tests drive
+    // the global-table path with it).
+    size_t smem_cap = 160 * 1024;
+    if (const char* env = getenv("GT_TC_TABLE_SMEM_MAX")) smem_cap = size_t(atoll(env));
+    int32_t* gtab = nullptr;
+    size_t smem = 0;
+    if (tab_bytes <= smem_cap) {
+      smem = tab_bytes;
+      if (smem > 48 * 1024)
+        GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_cta_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    } else {
+      gtab = ws_n<int32_t>(WS_TMP4, size_t(grid) << log_slots);
     }
-    Phase ph("tc.count", 4.0 * m);
-    GT_LAUNCH(gtd::tc_count_kernel, ctx().sm_count * 8, 256, 0, off_p, adj_p, items, n_items,
-              counters + 21, total);
+    GT_LAUNCH(gtd::tc_count_cta_kernel, grid, 256, smem, o.off_p, o.adj_p, off_m, nm,
+              tasks + n_bm + n_wt, n_ct, log_slots, gtab, total);
   }
   int64_t result = 0;
   d2h(&result, total, 8);
@@ -346,9 +800,21 @@ int64_t triangles(const gt_graph* g) {
 
 using namespace gt;
 
-extern "C" int gt_triangles(const gt_graph* g, int64_t* count) {
+extern "C" {
+
+int gt_triangles(const gt_graph* g, int64_t* count) {
   GT_API_BEGIN
   if (!count) fail(GT_EINVAL, "count must not be NULL");
   *count = triangles(g);
   GT_API_END
 }
+
+int gt_triangle_orientation(const gt_graph* g, int32_t* h_deg, int32_t* h_rank, int64_t* h_off_p,
+                            int32_t* h_adj_p, int64_t* m) {
+  GT_API_BEGIN
+  if (!m) fail(GT_EINVAL, "m must not be NULL");
+  triangle_orientation(g, h_deg, h_rank, h_off_p, h_adj_p, m);
+  GT_API_END
+}
+
+}  // extern "C"
