@@ -20,11 +20,12 @@
 //   5 N- (transpose)     keys v<<32 | arc, stable sort on the v bits -> for
 //                        every v the arcs (u,v), in u order, as (first index
 //                        of N+(u) after v, remaining length): the "suffix"
-//   6 count              task = (v, chunk of N-(v)). The N+(v) membership
-//                        structure is a shared-memory BITMAP over (v, n) when
-//                        n-1-v <= TC_BM_BITS (the top ranks, where R-MAT puts
-//                        nearly all the work), else a hash table (per warp,
-//                        or per CTA for large d+(v)). For every arc (u,v) the
+//   6 count              task = (v, chunk of N-(v)), one warp each. The N+(v)
+//                        membership structure is a per-warp shared-memory
+//                        BITMAP over (v, n) when n-1-v <= 2^16 (the top ranks,
+//                        where R-MAT puts nearly all the work: 94% at C3),
+//                        else a per-warp hash table (or per CTA for large
+//                        d+(v)). For every arc (u,v) the
 //                        warp probes the suffix of N+(u) after v — exactly
 //                        the w > v candidates — flattened across 32 lanes so
 //                        reads stay coalesced; each triangle u<v<w is counted
@@ -48,7 +49,7 @@ constexpr int TC_SLOTS = 2048;                 // hash slots per warp (8 KB)
 constexpr int TC_WARP_MAX = TC_SLOTS / 4;      // largest d+(v) of a warp hash task
 constexpr int TC_CHUNK = 256;                  // arcs per warp task
 constexpr int TC_CHUNK_CTA = 1024;             // arcs per CTA task
-constexpr int TC_BM_BITS = 1 << 18;            // bitmap window (32 KB of shared memory)
+constexpr int TC_BM_BITS = TC_SLOTS * 32;      // per-warp bitmap window (same 8 KB region)
 constexpr int32_t TC_EMPTY = -1;
 
 __global__ void __launch_bounds__(256) cat_off_kernel(const int64_t* __restrict__ out_off,
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(256) nminus_fill_kernel(const int32_t* __restr
 }
 
 // ---- work lists --------------------------------------------------------------
-// kind 0: bitmap CTA tasks (n-1-v <= TC_BM_BITS), 1: warp hash tasks,
+// kind 0: warp bitmap tasks (n-1-v <= TC_BM_BITS), 1: warp hash tasks,
 // 2: CTA hash tasks. A task is (v, chunk of N-(v)); it needs d+(v), d-(v) >= 1.
 __global__ void __launch_bounds__(256) tc_task_count_kernel(const int64_t* __restrict__ off_p,
                                                             const int64_t* __restrict__ off_m,
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(256) tc_task_count_kernel(const int64_t* __res
   const int64_t dm = off_m[v + 1] - off_m[v];
   const bool live = dp >= 1 && dm >= 1;
   const bool bm = n - 1 - v <= TC_BM_BITS;
-  c0[v] = (live && bm) ? (dm + TC_CHUNK_CTA - 1) / TC_CHUNK_CTA : 0;
+  c0[v] = (live && bm) ? (dm + TC_CHUNK - 1) / TC_CHUNK : 0;
   c1[v] = (live && !bm && dp <= TC_WARP_MAX) ? (dm + TC_CHUNK - 1) / TC_CHUNK : 0;
   c2[v] = (live && !bm && dp > TC_WARP_MAX) ? (dm + TC_CHUNK_CTA - 1) / TC_CHUNK_CTA : 0;
 }
@@ -367,13 +368,17 @@ struct HashProbe {
   }
 };
 
-// Bit (w - v - 1) of the window (v, v + 1 + bits) for every w in N+(v).
+// Bit (w - v - 1) of the window (v, v + 1 + bits) for every w in N+(v). The
+// bitmap is addressed through its 32-bit shared-window address so every
+// probe is one LDS (a generic pointer would cost the window translation).
 struct BitmapProbe {
-  const uint32_t* bm;
-  int32_t base;  // v + 1
+  uint32_t sbase;  // shared-space address of word 0
+  int32_t base;    // v + 1
   __device__ __forceinline__ bool operator()(int32_t w) const {
     const uint32_t i = uint32_t(w - base);
-    return (bm[i >> 5] >> (i & 31)) & 1u;
+    uint32_t x;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(sbase + ((i >> 5) << 2)) : "memory");
+    return (x >> (i & 31)) & 1u;
   }
 };
 
@@ -384,24 +389,75 @@ __device__ __forceinline__ int tc_log_slots(int64_t d, int cap_log) {
 }
 
 // One warp probes up to 32 suffixes (lane = arc (u,v): positions [s, s+len)
-// of adj, all w > v) against N+(v): position t of the concatenation of the 32
-// suffixes belongs to the lane whose suffix starts last at or before t, so
-// consecutive lanes read consecutive elements (coalesced) whatever the
-// lengths. TC_WIN windows of 32 positions are resolved per step and their
-// loads issued together (TC_WIN independent reads in flight per lane).
+// of adj, all w > v) against N+(v).
+//  * long suffixes (>= TC_LONG, ~97% of the probes on R-MAT) are walked by
+//    the whole warp one arc at a time, TC_UNROLL coalesced loads in flight;
+//  * the short rest is flattened: position t of the concatenation of the
+//    short suffixes belongs to the lane whose suffix starts last at or before
+//    t (position -> lane map in shared memory), TC_WIN windows of 32
+//    positions resolved per step, so lanes stay busy and reads coalesced.
 constexpr int TC_WIN = 4;
+constexpr int TC_LONG = 16;
+constexpr int TC_UNROLL = 4;
 
 template <typename Probe>
 __device__ __forceinline__ uint32_t tc_wedges32(const int32_t* __restrict__ adj, int2 suffix,
                                                 const Probe& probe,
                                                 uint8_t* s_start /* [32 * TC_WIN] */) {
   const int lane = threadIdx.x & 31;
+  uint32_t cnt = 0;
+  // ---- long suffixes: warp per arc; the first 32*TC_UNROLL positions of the
+  // NEXT arc are loaded before the current one is probed (software pipeline)
+  unsigned longs = __ballot_sync(0xffffffffu, suffix.y >= TC_LONG);
+  auto fetch = [&](int i, const int32_t*& b, int& l, int32_t (&w)[TC_UNROLL]) {
+    b = adj + __shfl_sync(0xffffffffu, suffix.x, i);
+    l = __shfl_sync(0xffffffffu, suffix.y, i);
+#pragma unroll
+    for (int q = 0; q < TC_UNROLL; ++q) {
+      const int k = 32 * q + lane;
+      w[q] = k < l ? __ldg(b + k) : TC_EMPTY;
+    }
+  };
+  if (longs) {
+    int32_t wa[TC_UNROLL], wb[TC_UNROLL];
+    const int32_t *ba, *bb = adj;
+    int la, lb = 0;
+    int i = __ffs(longs) - 1;
+    longs &= longs - 1;
+    fetch(i, ba, la, wa);
+    while (i >= 0) {
+      const int j = longs ? __ffs(longs) - 1 : -1;
+      if (j >= 0) {
+        longs &= longs - 1;
+        fetch(j, bb, lb, wb);
+      }
+#pragma unroll
+      for (int q = 0; q < TC_UNROLL; ++q)
+        if (wa[q] != TC_EMPTY) cnt += probe(wa[q]) ? 1u : 0u;
+      for (int k0 = 32 * TC_UNROLL; k0 < la; k0 += 32 * TC_UNROLL) {  // rare: long tails
+        int32_t w[TC_UNROLL];
+#pragma unroll
+        for (int q = 0; q < TC_UNROLL; ++q) {
+          const int k = k0 + 32 * q + lane;
+          w[q] = k < la ? __ldg(ba + k) : TC_EMPTY;
+        }
+#pragma unroll
+        for (int q = 0; q < TC_UNROLL; ++q)
+          if (w[q] != TC_EMPTY) cnt += probe(w[q]) ? 1u : 0u;
+      }
+      i = j;
+      ba = bb;
+      la = lb;
+#pragma unroll
+      for (int q = 0; q < TC_UNROLL; ++q) wa[q] = wb[q];
+    }
+  }
+  // ---- short suffixes: flattened across the lanes --------------------------
   const int64_t ou = suffix.x;
-  const int du = suffix.y;
+  const int du = suffix.y < TC_LONG ? suffix.y : 0;
   const int incl = warp_incl_scan(du);
   const int tot = __shfl_sync(0xffffffffu, incl, 31);
   const int excl = incl - du;
-  uint32_t cnt = 0;
   int carry = 0;
   for (int t0 = 0; t0 < tot; t0 += 32 * TC_WIN) {
     // suffixes starting in this step: position -> lane map + per-window masks
@@ -416,13 +472,15 @@ __device__ __forceinline__ uint32_t tc_wedges32(const int32_t* __restrict__ adj,
     int32_t w[TC_WIN];
 #pragma unroll
     for (int q = 0; q < TC_WIN; ++q) {
+      w[q] = TC_EMPTY;
+      if (t0 + 32 * q >= tot) continue;  // warp-uniform: nothing left
       const unsigned mine = starts[q] & (0xffffffffu >> (31 - lane));
       const int owner = mine ? int(s_start[32 * q + 31 - __clz(mine)]) : carry;
       carry = __shfl_sync(0xffffffffu, owner, 31);
       const int64_t o = __shfl_sync(0xffffffffu, ou, owner);
       const int ex = __shfl_sync(0xffffffffu, excl, owner);
       const int t = t0 + 32 * q + lane;
-      w[q] = t < tot ? __ldg(adj + o + (t - ex)) : TC_EMPTY;
+      if (t < tot) w[q] = __ldg(adj + o + (t - ex));
     }
 #pragma unroll
     for (int q = 0; q < TC_WIN; ++q)
@@ -432,60 +490,23 @@ __device__ __forceinline__ uint32_t tc_wedges32(const int32_t* __restrict__ adj,
   return cnt;
 }
 
-// Bitmap tasks: CTA per (v, chunk of N-(v)), bitmap of (v, n) in shared memory.
-__global__ void __launch_bounds__(256) tc_count_bitmap_kernel(
-    const int64_t* __restrict__ off_p, const int32_t* __restrict__ adj_p,
-    const int64_t* __restrict__ off_m, const int2* __restrict__ nm,
-    const int2* __restrict__ tasks, int64_t n_tasks, int64_t n,
-    unsigned long long* __restrict__ total) {
-  extern __shared__ uint32_t s_bm[];  // TC_BM_BITS / 32 words
-  __shared__ uint8_t s_start[8][32 * TC_WIN];
-  __shared__ unsigned long long s_red[8];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned long long acc = 0;
-  for (int64_t it = blockIdx.x; it < n_tasks; it += gridDim.x) {
-    const int2 task = tasks[it];
-    const int v = task.x;
-    const int64_t ov = off_p[v];
-    const int dv = int(off_p[v + 1] - ov);
-    const int nwords = int((n - 1 - v + 31) >> 5);
-    __syncthreads();  // previous task done with the bitmap
-    for (int i = threadIdx.x; i < nwords; i += 256) s_bm[i] = 0u;
-    __syncthreads();
-    for (int i = threadIdx.x; i < dv; i += 256) {
-      const uint32_t b = uint32_t(adj_p[ov + i] - v - 1);
-      atomicOr(&s_bm[b >> 5], 1u << (b & 31));
-    }
-    __syncthreads();
-    const BitmapProbe probe{s_bm, v + 1};
-    const int64_t om = off_m[v];
-    const int dm = int(off_m[v + 1] - om);
-    const int begin = task.y * TC_CHUNK_CTA;
-    const int end = min(dm, begin + TC_CHUNK_CTA);
-    uint32_t cnt = 0;
-    for (int jb = begin + warp * 32; jb < end; jb += 256) {
-      const int jj = jb + lane;
-      const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
-      cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
-    }
-    acc += cnt;
-  }
-  acc = block_sum_256(acc, s_red);
-  if (threadIdx.x == 0 && acc) atomicAdd(total, acc);
-}
-
-// Hash tasks, warp per (v, chunk): N+(v) in a per-warp table (load <= 1/4).
+// Warp per task (v, chunk of N-(v)), dynamic task grabbing. Each warp owns
+// an 8 KB shared-memory region that holds N+(v) either as a BITMAP of the
+// window (v, n) (kind 0: n-1-v <= TC_BM_BITS) or as a hash table (kind 1:
+// d+(v) <= TC_WARP_MAX, load <= 1/4). Tasks of the same v are adjacent in
+// the list, so a warp that draws the next chunk of its v reuses the table.
 __global__ void __launch_bounds__(256) tc_count_warp_kernel(
     const int64_t* __restrict__ off_p, const int32_t* __restrict__ adj_p,
     const int64_t* __restrict__ off_m, const int2* __restrict__ nm,
-    const int2* __restrict__ tasks, int64_t n_tasks, unsigned int* __restrict__ next_task,
-    unsigned long long* __restrict__ total) {
+    const int2* __restrict__ tasks, int64_t n_bitmap_tasks, int64_t n_tasks, int64_t n,
+    unsigned int* __restrict__ next_task, unsigned long long* __restrict__ total) {
   extern __shared__ int32_t s_tab[];  // [8][TC_SLOTS]
   __shared__ uint8_t s_start[8][32 * TC_WIN];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int32_t* tab = s_tab + warp * TC_SLOTS;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(tab);
   int cur_v = -1;
-  HashProbe probe{tab, 31u, 5};
+  HashProbe hprobe{tab, 31u, 5};
   unsigned long long acc = 0;
   while (true) {
     unsigned int it = 0;
@@ -494,14 +515,25 @@ __global__ void __launch_bounds__(256) tc_count_warp_kernel(
     if (int64_t(it) >= n_tasks) break;
     const int2 task = tasks[it];
     const int v = task.x;
+    const bool use_bm = int64_t(it) < n_bitmap_tasks;
     if (v != cur_v) {
       const int64_t ov = off_p[v];
       const int dv = int(off_p[v + 1] - ov);
-      probe.log_slots = tc_log_slots(dv, 11);
-      probe.mask = (1u << probe.log_slots) - 1u;
-      for (int i = lane; i <= int(probe.mask); i += 32) tab[i] = TC_EMPTY;
-      __syncwarp();
-      for (int i = lane; i < dv; i += 32) probe.insert(adj_p[ov + i]);
+      if (use_bm) {
+        const int nwords = int((n - 1 - v + 31) >> 5);
+        for (int i = lane; i < nwords; i += 32) bm[i] = 0u;
+        __syncwarp();
+        for (int i = lane; i < dv; i += 32) {
+          const uint32_t b = uint32_t(adj_p[ov + i] - v - 1);
+          atomicOr(&bm[b >> 5], 1u << (b & 31));
+        }
+      } else {
+        hprobe.log_slots = tc_log_slots(dv, 11);
+        hprobe.mask = (1u << hprobe.log_slots) - 1u;
+        for (int i = lane; i <= int(hprobe.mask); i += 32) tab[i] = TC_EMPTY;
+        __syncwarp();
+        for (int i = lane; i < dv; i += 32) hprobe.insert(adj_p[ov + i]);
+      }
       __syncwarp();
       cur_v = v;
     }
@@ -509,10 +541,19 @@ __global__ void __launch_bounds__(256) tc_count_warp_kernel(
     const int dm = int(off_m[v + 1] - om);
     const int end = min(dm, (task.y + 1) * TC_CHUNK);
     uint32_t cnt = 0;
-    for (int jb = task.y * TC_CHUNK; jb < end; jb += 32) {
-      const int jj = jb + lane;
-      const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
-      cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
+    if (use_bm) {
+      const BitmapProbe probe{uint32_t(__cvta_generic_to_shared(bm)), v + 1};
+      for (int jb = task.y * TC_CHUNK; jb < end; jb += 32) {
+        const int jj = jb + lane;
+        const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
+        cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
+      }
+    } else {
+      for (int jb = task.y * TC_CHUNK; jb < end; jb += 32) {
+        const int jj = jb + lane;
+        const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
+        cnt += tc_wedges32(adj_p, sfx, hprobe, s_start[warp]);
+      }
     }
     acc += cnt;
   }
@@ -747,25 +788,14 @@ int64_t triangles(const gt_graph* g) {
   GT_CUDA(cudaMemsetAsync(total, 0, 8, s));
   // algorithmic bytes credited: every N- entry and N+ list once (the probed
   // suffix elements depend on the graph and are not counted)
-  if (n_bm) {
+  if (n_bm + n_wt) {
     Phase ph("tc.count", 8.0 * m + 4.0 * m);
-    const int words = int((std::min<int64_t>(n, gtd::TC_BM_BITS) + 31) / 32);
-    const int smem = words * 4;
-    if (smem > 48 * 1024)
-      GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_bitmap_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int grid = static_cast<int>(std::min<int64_t>(n_bm, 6LL * ctx().sm_count));
-    GT_LAUNCH(gtd::tc_count_bitmap_kernel, grid, 256, smem, o.off_p, o.adj_p, off_m, nm, tasks,
-              n_bm, n, total);
-  }
-  if (n_wt) {
-    Phase ph("tc.count_hash", 0.0);
     GT_CUDA(cudaMemsetAsync(counters + 22, 0, 4, s));
     const int smem = 8 * gtd::TC_SLOTS * 4;
     GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_warp_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     GT_LAUNCH(gtd::tc_count_warp_kernel, ctx().sm_count * 3, 256, smem, o.off_p, o.adj_p, off_m,
-              nm, tasks + n_bm, n_wt, counters + 22, total);
+              nm, tasks, n_bm, n_bm + n_wt, n, counters + 22, total);
   }
   if (n_ct) {
     Phase ph("tc.count_hash", 0.0);
