@@ -2,6 +2,8 @@
 #include "radix_sort.cuh"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 namespace gtd {
 
@@ -33,14 +35,22 @@ __global__ void __launch_bounds__(256) digit_scan_kernel(const unsigned long lon
   base[q * 256 + threadIdx.x] = ex;
 }
 
+// One onesweep LSD pass over a BITS-wide digit (BITS is a template parameter
+// so the per-bit ballot loop is fully unrolled). RS_MATCH of the RS_KPT keys
+// of a thread are ranked with __match_any_sync (ADU pipe), the rest with one
+// ballot per digit bit (ALU pipe): splitting the ranking across the two pipes
+// keeps either from being the bottleneck (ncu: all-MATCH ranking was 68%
+// ADU-bound, all-ballot ranking doubled the instruction count).
+template <int BITS, int RS_MATCH>
 __global__ void __launch_bounds__(RS_THREADS, 3)
     onesweep_kernel(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int64_t n,
-                    int shift, int bits, const int64_t* __restrict__ digit_base,
+                    int shift, const int64_t* __restrict__ digit_base,
                     uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter,
                     uint32_t epoch) {
   constexpr int NW = RS_THREADS / 32;
-  __shared__ union {
-    uint64_t keys[RS_TILE];
+  constexpr uint32_t mask = (1u << BITS) - 1u;
+  __shared__ struct {
+    uint64_t keys[RS_TILE];  // staged by index during the look-back, then by position
     uint32_t whist[NW][256];
   } s;
   __shared__ int64_t s_gbase[256];
@@ -53,38 +63,57 @@ __global__ void __launch_bounds__(RS_THREADS, 3)
   __syncthreads();
   const int tile = int(s_tile);
   const int64_t base = int64_t(tile) * RS_TILE;
-  const int64_t wbase = base + int64_t(warp) * 32 * RS_KPT;
-  const uint32_t mask = (1u << bits) - 1u;
+  const int woff = warp * 32 * RS_KPT + lane;  // key i of this thread: tile element woff + 32*i
 
+  const int64_t rem64 = n - (base + woff);
+  const int rem = rem64 > 32 * RS_KPT ? 32 * RS_KPT : (rem64 < 0 ? 0 : int(rem64));
+  const uint64_t* src = in + (base + woff);
   uint64_t k[RS_KPT];
 #pragma unroll
-  for (int i = 0; i < RS_KPT; ++i) {
-    const int64_t idx = wbase + i * 32 + lane;
-    k[i] = idx < n ? ld_stream_u64(in + idx) : ~0ull;
-  }
+  for (int i = 0; i < RS_KPT; ++i) k[i] = 32 * i < rem ? ld_stream_u64(src + 32 * i) : ~0ull;
 
-  // Warp-level multi-split: rank every key among the equal digits of its
-  // warp in lane order (stable). __match_any_sync finds the peers of a digit
-  // in one instruction; invalid tail keys match only each other (digit 256).
+  // Peer masks: lanes of this warp whose key i has the same digit (invalid
+  // tail keys are in no mask).
   uint32_t rank[RS_KPT];
   const unsigned lt = lanemask_lt();
 #pragma unroll
   for (int i = 0; i < RS_KPT; ++i) {
-    const bool valid = (wbase + i * 32 + lane) < n;
-    const uint32_t d = valid ? uint32_t(k[i] >> shift) & mask : 256u;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    uint32_t before = 0;
-    if (valid) before = s.whist[warp][d];
-    rank[i] = before + __popc(peers & lt);
-    const int leader = 31 - __clz(peers);
-    __syncwarp();
-    if (valid && lane == leader) s.whist[warp][d] = before + __popc(peers);
-    __syncwarp();
+    const uint32_t d = uint32_t(k[i] >> shift) & mask;
+    if (i < RS_MATCH) {
+      rank[i] = __match_any_sync(0xffffffffu, 32 * i < rem ? d : 0xFFFFu) &
+                __ballot_sync(0xffffffffu, 32 * i < rem);
+    } else {
+      uint32_t peers = __ballot_sync(0xffffffffu, 32 * i < rem);
+#pragma unroll
+      for (int b = 0; b < BITS; ++b) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bal : ~bal;
+      }
+      rank[i] = peers;
+    }
   }
+  // Stable ranks: key by key, the highest peer adds the group size to the
+  // warp's private counter with one shared atomic; the old value is
+  // broadcast to the group.
+  uint32_t* wh = s.whist[warp];
+#pragma unroll
+  for (int i = 0; i < RS_KPT; ++i) {
+    const uint32_t peers = rank[i];
+    const int leader = 31 - __clz(peers);
+    uint32_t before = 0;
+    if (32 * i < rem && lane == leader)
+      before = atomicAdd(&wh[uint32_t(k[i] >> shift) & mask], __popc(peers));
+    before = __shfl_sync(0xffffffffu, before, leader);
+    rank[i] = before + __popc(peers & lt);
+  }
+  // park the keys in shared memory (by index) so that they do not hold 32
+  // registers across the look-back
+#pragma unroll
+  for (int i = 0; i < RS_KPT; ++i) s.keys[woff + 32 * i] = k[i];
   __syncthreads();
 
   // Per digit (thread == digit): warp offsets, tile count, look-back.
-  {
+  if (tid < (1 << BITS)) {
     const int d = tid;
     uint32_t run = 0;
 #pragma unroll
@@ -97,46 +126,63 @@ __global__ void __launch_bounds__(RS_THREADS, 3)
     uint64_t* st = status + int64_t(tile) * 256 + d;
     if (tile == 0) st_status_u64(st, lb_pack(LB_INC, epoch, tile_cnt));
     else st_status_u64(st, lb_pack(LB_AGG, epoch, tile_cnt));
-
-    uint32_t tot;
-    const uint32_t local_start = block_excl_scan_256<uint32_t>(tile_cnt, s_scan, tot);
-
+    s.whist[0][d] = run;  // tile count, for the in-tile digit scan below (w=0 offset is 0)
+    // Decoupled look-back, LB_WIN predecessors polled per round trip.
     uint64_t excl = 0;
     if (tile > 0) {
+      constexpr int LB_WIN = 4;
       const uint64_t ep = uint64_t(epoch & 0x3FFFFFu);
       int t = tile - 1;
-      while (true) {
-        const uint64_t v = ld_status_u64(status + int64_t(t) * 256 + d);
-        if (((v >> 40) & 0x3FFFFFu) != ep || (v >> 62) == 0) continue;
-        excl += v & ((1ull << 40) - 1);
-        if ((v >> 62) == 2) break;
-        --t;
+      bool done = false;
+      while (!done) {
+        uint64_t v[LB_WIN];
+#pragma unroll
+        for (int q = 0; q < LB_WIN; ++q)
+          v[q] = t - q >= 0 ? ld_status_u64(status + int64_t(t - q) * 256 + d) : 0ull;
+#pragma unroll
+        for (int q = 0; q < LB_WIN; ++q) {
+          if (done || t < 0) break;
+          if (((v[q] >> 40) & 0x3FFFFFu) != ep || (v[q] >> 62) == 0) break;  // re-poll
+          excl += v[q] & ((1ull << 40) - 1);
+          if ((v[q] >> 62) == 2) done = true;
+          else --t;
+        }
       }
       st_status_u64(st, lb_pack(LB_INC, epoch, excl + tile_cnt));
     }
-    s_gbase[d] = digit_base[d] + int64_t(excl) - int64_t(local_start);
+    s_gbase[d] = digit_base[d] + int64_t(excl);
+  }
+  __syncthreads();
+  // in-tile digit starts (exclusive scan of the tile counts over the digits)
+  {
+    const uint32_t c = tid < (1 << BITS) ? s.whist[0][tid] : 0u;
+    uint32_t tot;
+    const uint32_t start = block_excl_scan_256<uint32_t>(c, s_scan, tot);
+    if (tid < (1 << BITS)) {
+      s.whist[0][tid] = 0;
+      s_gbase[tid] -= int64_t(start);
 #pragma unroll
-    for (int w = 0; w < NW; ++w) s.whist[w][d] += local_start;
+      for (int w = 0; w < NW; ++w) s.whist[w][tid] += start;
+    }
   }
   __syncthreads();
 
   uint32_t pos[RS_KPT];
 #pragma unroll
   for (int i = 0; i < RS_KPT; ++i) {
-    const uint32_t d = uint32_t(k[i] >> shift) & mask;
-    pos[i] = s.whist[warp][d] + rank[i];
+    k[i] = s.keys[woff + 32 * i];
+    pos[i] = s.whist[warp][uint32_t(k[i] >> shift) & mask] + rank[i];
   }
-  __syncthreads();  // whist aliases the key staging buffer
+  __syncthreads();  // every key read back before the buffer is reused by position
 #pragma unroll
   for (int i = 0; i < RS_KPT; ++i)
-    if (wbase + i * 32 + lane < n) s.keys[pos[i]] = k[i];
+    if (32 * i < rem) s.keys[pos[i]] = k[i];
   __syncthreads();
 
   const int nvalid = (n - base) < RS_TILE ? int(n - base) : RS_TILE;
   for (int j = tid; j < nvalid; j += RS_THREADS) {
     const uint64_t key = s.keys[j];
-    const uint32_t d = uint32_t(key >> shift) & mask;
-    out[s_gbase[d] + j] = key;
+    out[s_gbase[uint32_t(key >> shift) & mask] + j] = key;
   }
 }
 
@@ -176,6 +222,46 @@ void sort_histogram(const uint64_t* keys, int64_t n, const SortPlan& plan, SortH
   GT_LAUNCH(gtd::hist_kernel, grid, 256, 0, keys, n, plan, h.hist);
 }
 
+template <int BITS, int M>
+static void launch_bits(int grid, const uint64_t* src, uint64_t* dst, int64_t n, int shift,
+                        const int64_t* digit_base, uint64_t* status, uint32_t* counter,
+                        uint32_t epoch) {
+  GT_LAUNCH((gtd::onesweep_kernel<BITS, M>), grid, RS_THREADS, 0, src, dst, n, shift, digit_base,
+            status, counter, epoch);
+}
+
+template <int M>
+static void launch_m(int bits, int grid, const uint64_t* src, uint64_t* dst, int64_t n, int shift,
+                     const int64_t* digit_base, uint64_t* status, uint32_t* counter,
+                     uint32_t epoch) {
+  switch (bits) {
+    case 1: launch_bits<1, M>(grid, src, dst, n, shift, digit_base, status, counter, epoch); break;
+    case 2: launch_bits<2, M>(grid, src, dst, n, shift, digit_base, status, counter, epoch); break;
+    case 3: launch_bits<3, M>(grid, src, dst, n, shift, digit_base, status, counter, epoch); break;
+    case 4: launch_bits<4, M>(grid, src, dst, n, shift, digit_base, status, counter, epoch); break;
+    case 5: launch_bits<5, M>(grid, src, dst, n, shift, digit_base, status, counter, epoch); break;
+    case 6: launch_bits<6, M>(grid, src, dst, n, shift, digit_base, status, counter, epoch); break;
+    case 7: launch_bits<7, M>(grid, src, dst, n, shift, digit_base, status, counter, epoch); break;
+    case 8: launch_bits<8, M>(grid, src, dst, n, shift, digit_base, status, counter, epoch); break;
+    default: fail(GT_EINVAL, "radix digit width must be 1..8");
+  }
+}
+
+static void launch_onesweep(int bits, int nmatch, int grid, const uint64_t* src, uint64_t* dst,
+                            int64_t n, int shift, const int64_t* digit_base, uint64_t* status,
+                            uint32_t* counter, uint32_t epoch) {
+  if (nmatch <= 0)
+    launch_m<0>(bits, grid, src, dst, n, shift, digit_base, status, counter, epoch);
+  else if (nmatch >= RS_KPT)
+    launch_m<RS_KPT>(bits, grid, src, dst, n, shift, digit_base, status, counter, epoch);
+  else if (nmatch <= 6)
+    launch_m<6>(bits, grid, src, dst, n, shift, digit_base, status, counter, epoch);
+  else if (nmatch <= 8)
+    launch_m<8>(bits, grid, src, dst, n, shift, digit_base, status, counter, epoch);
+  else
+    launch_m<11>(bits, grid, src, dst, n, shift, digit_base, status, counter, epoch);
+}
+
 uint64_t* radix_sort(uint64_t* a, uint64_t* b, int64_t n, const SortPlan& plan, SortHist h,
                      const char* phase) {
   if (n <= 1 || plan.passes == 0) return a;
@@ -190,11 +276,16 @@ uint64_t* radix_sort(uint64_t* a, uint64_t* b, int64_t n, const SortPlan& plan, 
   }
   uint64_t* src = a;
   uint64_t* dst = b;
+  static int nmatch = -1;
+  if (nmatch < 0) {  // GT_SORT_MATCH: keys per thread ranked by __match_any_sync (tuning)
+    const char* env = getenv("GT_SORT_MATCH");
+    nmatch = env ? atoi(env) : 6;
+  }
   for (int q = 0; q < plan.passes; ++q) {
     Phase ph(phase, 16.0 * n);
     const uint32_t epoch = next_epoch();
-    GT_LAUNCH(gtd::onesweep_kernel, static_cast<int>(tiles), RS_THREADS, 0, src, dst, n,
-              plan.shift[q], plan.bits[q], h.digit_base + q * 256, status, counters + q, epoch);
+    launch_onesweep(plan.bits[q], nmatch, static_cast<int>(tiles), src, dst, n, plan.shift[q],
+                    h.digit_base + q * 256, status, counters + q, epoch);
     std::swap(src, dst);
   }
   return src;
