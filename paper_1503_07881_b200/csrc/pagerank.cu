@@ -19,6 +19,12 @@
 //   pr_fixup_kernel  finishes the rows that span tiles (tail + heads of the
 //                    following tiles, fixed order) and reduces the dangling
 //                    mass of the new scores (fixed tree + last-block combine).
+// Source relabelling (setup, once per call): nodes are renumbered by
+// descending out-degree (pos[v]); the in-adjacency is rewritten in that
+// numbering and the contrib vector is kept in it, so the contributions of the
+// hub sources — which R-MAT puts behind most edges (C2: the top 16K sources
+// feed 41% of the edges) — sit in a few hundred KB that stays in L1/L2
+// instead of being spread over the whole vector. Scores stay in id order.
 // HBM traffic per iteration (algorithmic): 4E (in_adj) + 8E (contrib gathers)
 // + 8(N+1) (in_off) + 8N (inv_out) + 8N (contrib write) [+ 8N score, last
 // iteration only].
@@ -57,6 +63,7 @@ __device__ __forceinline__ void grid_reduce_last(double block_val, double* parti
 }
 
 __global__ void __launch_bounds__(256) pr_init_kernel(const int64_t* __restrict__ out_off, int64_t n,
+                                                      const int32_t* __restrict__ pos,
                                                       double* __restrict__ inv_out,
                                                       double* __restrict__ contrib,
                                                       double* __restrict__ partials,
@@ -70,11 +77,57 @@ __global__ void __launch_bounds__(256) pr_init_kernel(const int64_t* __restrict_
     const int64_t deg = out_off[v + 1] - out_off[v];
     const double inv = deg ? 1.0 / double(deg) : 0.0;
     inv_out[v] = inv;
-    contrib[v] = s0 * inv;
+    contrib[pos[v]] = s0 * inv;
     if (deg == 0) dang += s0;
   }
   dang = block_sum_256(dang, s_red);
   grid_reduce_last(dang, partials, ticket, dangling0);
+}
+
+// Relabelling keys: (max_deg - outdeg(v)) << kbits | v  -> ascending sort =
+// descending out-degree, ties by id.
+__global__ void __launch_bounds__(256) pr_relabel_keys_kernel(const int64_t* __restrict__ out_off,
+                                                              int64_t n, int64_t max_deg, int kbits,
+                                                              gt::SortPlan plan,
+                                                              unsigned long long* __restrict__ hist,
+                                                              uint64_t* __restrict__ keys) {
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
+  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+    const uint64_t k = (uint64_t(max_deg - (out_off[v + 1] - out_off[v])) << kbits) | uint64_t(v);
+    keys[v] = k;
+    plan_hist_add(sh, plan, k);
+  }
+  __syncthreads();
+  plan_hist_flush(sh, plan, hist);
+}
+
+__global__ void __launch_bounds__(256) pr_pos_kernel(const uint64_t* __restrict__ sorted, int64_t n,
+                                                     uint64_t lowmask, int32_t* __restrict__ pos) {
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p < n) pos[sorted[p] & lowmask] = int32_t(p);
+}
+
+__global__ void __launch_bounds__(256) pr_remap_kernel(const int32_t* __restrict__ in_adj, int64_t e,
+                                                       const int32_t* __restrict__ pos,
+                                                       int32_t* __restrict__ out) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < e; i += stride)
+    out[i] = pos[__ldcs(in_adj + i)];
+}
+
+__global__ void __launch_bounds__(256) pr_max_outdeg_kernel(const int64_t* __restrict__ out_off,
+                                                            int64_t n,
+                                                            unsigned long long* __restrict__ out) {
+  unsigned long long mx = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+    mx = max(mx, (unsigned long long)(out_off[v + 1] - out_off[v]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
 }
 
 // tile_row[c] = first row whose in-edges start at or after c*PR_TILE.
@@ -94,11 +147,23 @@ __global__ void __launch_bounds__(256) pr_tile_rows_kernel(const int64_t* __rest
   tile_row[c] = lo;
 }
 
+constexpr int PR_ROWCAP = 512;   // rows of a tile whose metadata is staged on chip
+
+// Per-tile row metadata in shared memory: relative start of every segment
+// (clamped to the tile), 1/outdeg and the relabelled position of its row.
+struct PrRows {
+  uint16_t off[PR_ROWCAP + 1];
+  double inv[PR_ROWCAP];
+  int32_t pos[PR_ROWCAP];
+};
+
 template <int G>
-__device__ __forceinline__ void pr_rows(const double* vals, const int64_t* __restrict__ in_off,
-                                        int64_t e0, int64_t e1, int64_t ra, int64_t rb,
-                                        bool has_head, int64_t c, double base, double damping,
+__device__ __forceinline__ void pr_rows(const double* vals, const PrRows& sr,
+                                        const int64_t* __restrict__ in_off, int64_t e0, int ne,
+                                        int64_t first_row, int64_t nseg, bool has_head,
+                                        bool has_tail, int64_t c, double base, double damping,
                                         const double* __restrict__ inv_out,
+                                        const int32_t* __restrict__ pos,
                                         double* __restrict__ score, double* __restrict__ contrib_next,
                                         double* __restrict__ head, double* __restrict__ tail,
                                         int64_t* __restrict__ tail_row, bool last_iter,
@@ -106,32 +171,35 @@ __device__ __forceinline__ void pr_rows(const double* vals, const int64_t* __res
   constexpr int GPW = 32 / G;  // groups per warp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / G, gl = lane % G;
-  const int64_t nseg = (rb - ra) + (has_head ? 1 : 0);
-  const int64_t first_row = has_head ? ra - 1 : ra;
+  auto off_at = [&](int64_t r) -> int {
+    if (r < PR_ROWCAP + 1) return sr.off[r];
+    const int64_t x = in_off[first_row + r] - e0;
+    return int(x < 0 ? 0 : (x > ne ? ne : x));
+  };
   for (int64_t s0 = int64_t(warp) * GPW; s0 < nseg; s0 += int64_t(PR_THREADS / 32) * GPW) {
     const int64_t s = s0 + grp;
     const bool active = s < nseg;
-    const int64_t row = first_row + s;
-    int64_t a = 0, b = 0;
+    int a = 0, b = 0;
     if (active) {
-      a = max(in_off[row], e0) - e0;
-      b = min(in_off[row + 1], e1) - e0;
+      a = off_at(s);
+      b = off_at(s + 1);
     }
     double sum = 0.0;
-    for (int64_t j = a + gl; j < b; j += G) sum += vals[j];
+    for (int j = a + gl; j < b; j += G) sum += vals[j];
     __syncwarp();
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (active && gl == 0) {
+      const int64_t row = first_row + s;
       if (has_head && s == 0) {
         head[c] = sum;
-      } else if (in_off[row + 1] > e1) {
+      } else if (has_tail && s == nseg - 1) {
         tail[c] = sum;
         tail_row[c] = row;
       } else {
         const double sc = base + damping * sum;
-        const double inv = inv_out[row];
-        if (!last_iter) contrib_next[row] = sc * inv;
+        const double inv = s < PR_ROWCAP ? sr.inv[s] : inv_out[row];
+        if (!last_iter) contrib_next[s < PR_ROWCAP ? sr.pos[s] : pos[row]] = sc * inv;
         else score[row] = sc;
         if (inv == 0.0) dang += sc;
       }
@@ -142,11 +210,13 @@ __device__ __forceinline__ void pr_rows(const double* vals, const int64_t* __res
 __global__ void __launch_bounds__(PR_THREADS) pr_spmv_kernel(
     const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_adj, int64_t n, int64_t e,
     const int64_t* __restrict__ tile_row, const double* __restrict__ contrib,
-    const double* __restrict__ inv_out, const double* __restrict__ dangling_prev, double damping,
+    const double* __restrict__ inv_out, const int32_t* __restrict__ pos,
+    const double* __restrict__ dangling_prev, double damping,
     double* __restrict__ score, double* __restrict__ contrib_next, double* __restrict__ head,
     double* __restrict__ tail, int64_t* __restrict__ tail_row, double* __restrict__ dpart,
     int last_iter) {
   __shared__ double vals[PR_TILE];
+  __shared__ PrRows sr;
   __shared__ double s_red[8];
   const int64_t c = blockIdx.x;
   const int64_t e0 = c * PR_TILE;
@@ -155,14 +225,31 @@ __global__ void __launch_bounds__(PR_THREADS) pr_spmv_kernel(
   const int64_t ra = tile_row[c], rb = tile_row[c + 1];
   const double base = (1.0 - damping) / double(n) + damping * (*dangling_prev / double(n));
   if (threadIdx.x == 0) tail_row[c] = -1;
+  // segments: the head row ra-1 (starts before the tile) when it reaches
+  // into it, then rows ra..rb-1 (start inside); the last may run past e1
+  const bool has_head = ne > 0 && (ra == n || in_off[ra] > e0);
+  const int64_t first_row = has_head ? ra - 1 : ra;
+  const int64_t nseg = rb - first_row;
+  const bool has_tail = nseg > 0 && in_off[rb] > e1 && !(has_head && nseg == 1);
 
-  // Gather phase: PR_TILE/256 independent loads per thread in flight.
+  // Gather phase: PR_TILE/256 independent loads per thread in flight, and
+  // the tile's row metadata staged alongside (independent of the gathers).
   constexpr int PER = PR_TILE / PR_THREADS;
   int32_t idx[PER];
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const int j = i * PR_THREADS + threadIdx.x;
     idx[i] = j < ne ? __ldcs(in_adj + e0 + j) : 0;
+  }
+  const int64_t nstage = min(nseg + 1, int64_t(PR_ROWCAP + 1));
+  for (int64_t r = threadIdx.x; r < nstage; r += PR_THREADS) {
+    const int64_t row = first_row + r;
+    const int64_t x = in_off[row] - e0;
+    sr.off[r] = uint16_t(x < 0 ? 0 : (x > ne ? ne : x));
+    if (r < nseg && r < PR_ROWCAP) {
+      sr.inv[r] = inv_out[row];
+      sr.pos[r] = pos[row];
+    }
   }
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
@@ -171,33 +258,26 @@ __global__ void __launch_bounds__(PR_THREADS) pr_spmv_kernel(
   }
   __syncthreads();
 
-  const bool has_head = ne > 0 && (ra == n || in_off[ra] > e0);
-  const int64_t nseg = (rb - ra) + (has_head ? 1 : 0);
   const int64_t avg = nseg > 0 ? int64_t(ne) / nseg : 32;
   const bool last = last_iter != 0;
   double dang = 0.0;
-  if (avg >= 24)
-    pr_rows<32>(vals, in_off, e0, e1, ra, rb, has_head, c, base, damping, inv_out, score,
-                contrib_next, head, tail, tail_row, last, dang);
-  else if (avg >= 12)
-    pr_rows<16>(vals, in_off, e0, e1, ra, rb, has_head, c, base, damping, inv_out, score,
-                contrib_next, head, tail, tail_row, last, dang);
-  else if (avg >= 6)
-    pr_rows<8>(vals, in_off, e0, e1, ra, rb, has_head, c, base, damping, inv_out, score,
-               contrib_next, head, tail, tail_row, last, dang);
-  else if (avg >= 3)
-    pr_rows<4>(vals, in_off, e0, e1, ra, rb, has_head, c, base, damping, inv_out, score,
-               contrib_next, head, tail, tail_row, last, dang);
-  else
-    pr_rows<2>(vals, in_off, e0, e1, ra, rb, has_head, c, base, damping, inv_out, score,
-               contrib_next, head, tail, tail_row, last, dang);
+#define PR_ROWS(G)                                                                            \
+  pr_rows<G>(vals, sr, in_off, e0, ne, first_row, nseg, has_head, has_tail, c, base, damping, \
+             inv_out, pos, score, contrib_next, head, tail, tail_row, last, dang)
+  if (avg >= 24) PR_ROWS(32);
+  else if (avg >= 12) PR_ROWS(16);
+  else if (avg >= 6) PR_ROWS(8);
+  else if (avg >= 3) PR_ROWS(4);
+  else PR_ROWS(2);
+#undef PR_ROWS
   dang = block_sum_256(dang, s_red);
   if (threadIdx.x == 0) dpart[c] = dang;
 }
 
 __global__ void __launch_bounds__(256) pr_fixup_kernel(
     const int64_t* __restrict__ in_off, int64_t n, int64_t tiles,
-    const double* __restrict__ inv_out, const double* __restrict__ dangling_prev, double damping,
+    const double* __restrict__ inv_out, const int32_t* __restrict__ pos,
+    const double* __restrict__ dangling_prev, double damping,
     const double* __restrict__ head, const double* __restrict__ tail,
     const int64_t* __restrict__ tail_row, const double* __restrict__ dpart,
     double* __restrict__ score, double* __restrict__ contrib_next, int last_iter,
@@ -217,7 +297,7 @@ __global__ void __launch_bounds__(256) pr_fixup_kernel(
       const double sc = base + damping * sum;
       const double inv = inv_out[v];
       if (last_iter) score[v] = sc;
-      else contrib_next[v] = sc * inv;
+      else contrib_next[pos[v]] = sc * inv;
       if (inv == 0.0) dang += sc;
     }
   }
@@ -257,11 +337,44 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
   double* partials = reinterpret_cast<double*>(carve(size_t(std::max(fix_blocks, init_blocks)) * 8));
   unsigned int* ticket = reinterpret_cast<unsigned int*>(carve(16));
   double* score = on_device ? scores : dalloc_n<double>(n);
+  int32_t* pos = ws_n<int32_t>(WS_TMP4, size_t(n));
+  int32_t* in_adj_r = ws_n<int32_t>(WS_TMP2, size_t(e) + 1);
+  unsigned long long* maxd = reinterpret_cast<unsigned long long*>(ws_n<int64_t>(WS_SMALL, 16) + 13);
+
+  // Source relabelling by descending out-degree (see the header comment).
+  GT_CUDA(cudaMemsetAsync(maxd, 0, 8, ctx().stream));
+  {
+    Phase ph("pr.relabel", 8.0 * (n + 1));
+    GT_LAUNCH(gtd::pr_max_outdeg_kernel, init_blocks, 256, 0, g->out_off, n, maxd);
+  }
+  int64_t max_deg = 0;
+  d2h(&max_deg, maxd, 8);
+  sync();
+  {
+    const int kb = bits_for(n);
+    SortPlan plan = make_plan(0, kb + bits_for(max_deg + 1));
+    SortHist h = sort_hist_begin(0);
+    uint64_t* ka = ws_n<uint64_t>(WS_KEYS_A, size_t(n));
+    uint64_t* kb_ = ws_n<uint64_t>(WS_KEYS_B, size_t(n));
+    {
+      Phase ph("pr.relabel", 8.0 * (n + 1) + 8.0 * n);
+      GT_LAUNCH(gtd::pr_relabel_keys_kernel, init_blocks, 256, 0, g->out_off, n, max_deg, kb, plan,
+                h.hist, ka);
+    }
+    uint64_t* sorted = radix_sort(ka, kb_, n, plan, h, "pr.relabel");
+    Phase ph("pr.relabel", 12.0 * n + 12.0 * e);
+    GT_LAUNCH(gtd::pr_pos_kernel, ceil_div(n, 256), 256, 0, sorted, n, (uint64_t(1) << kb) - 1,
+              pos);
+    if (e > 0)
+      GT_LAUNCH(gtd::pr_remap_kernel, static_cast<int>(std::min<int64_t>(ceil_div64(e, 1024),
+                                                                         8LL * ctx().sm_count)),
+                256, 0, g->in_adj, e, pos, in_adj_r);
+  }
 
   GT_CUDA(cudaMemsetAsync(ticket, 0, 16, ctx().stream));
   {
-    Phase ph("pr.setup", 8.0 * (n + 1) + 16.0 * n + 8.0 * (tiles + 1));
-    GT_LAUNCH(gtd::pr_init_kernel, init_blocks, 256, 0, g->out_off, n, inv_out, contrib[0],
+    Phase ph("pr.setup", 8.0 * (n + 1) + 20.0 * n + 8.0 * (tiles + 1));
+    GT_LAUNCH(gtd::pr_init_kernel, init_blocks, 256, 0, g->out_off, n, pos, inv_out, contrib[0],
               partials, ticket, dang);
     GT_LAUNCH(gtd::pr_tile_rows_kernel, ceil_div(tiles + 1, 256), 256, 0, g->in_off, n, tiles,
               tile_row);
@@ -271,16 +384,16 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
     double* cur = contrib[it & 1];
     double* nxt = contrib[(it + 1) & 1];
     {
-      Phase ph("pr.spmv", 12.0 * e + 8.0 * (n + 1) + 16.0 * n + (last ? 0.0 : 0.0));
+      Phase ph("pr.spmv", 12.0 * e + 8.0 * (n + 1) + 20.0 * n);
       GT_LAUNCH(gtd::pr_spmv_kernel, static_cast<int>(tiles), gtd::PR_THREADS, 0, g->in_off,
-                g->in_adj, n, e, tile_row, cur, inv_out, dang + it, damping, score, nxt, head,
+                in_adj_r, n, e, tile_row, cur, inv_out, pos, dang + it, damping, score, nxt, head,
                 tail, tail_row, dpart, last);
     }
     {
       Phase ph("pr.fixup", 40.0 * tiles);
-      GT_LAUNCH(gtd::pr_fixup_kernel, fix_blocks, 256, 0, g->in_off, n, tiles, inv_out, dang + it,
-                damping, head, tail, tail_row, dpart, score, nxt, last, partials, ticket,
-                dang + it + 1);
+      GT_LAUNCH(gtd::pr_fixup_kernel, fix_blocks, 256, 0, g->in_off, n, tiles, inv_out, pos,
+                dang + it, damping, head, tail, tail_row, dpart, score, nxt, last, partials,
+                ticket, dang + it + 1);
     }
   }
   if (!on_device) {
