@@ -50,6 +50,8 @@ def parse_args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-rows", type=int, default=1_000_000)
+    p.add_argument("--sharded", action="store_true",
+                   help="use the multi-GPU (distributed.py) pipeline even on one GPU")
     return p.parse_args()
 
 
@@ -66,6 +68,12 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     return rank, world, local
+
+
+def dist_ready():
+    import torch.distributed as dist
+
+    return dist.is_available() and dist.is_initialized()
 
 
 def spec_for(name):
@@ -216,22 +224,42 @@ def ours_arm(args):
 
     spec = spec_for(args.config)
     dev = torch.device("cuda", local)
-    src, dst = rmat_device(spec, device=f"cuda:{local}")
+    # weak scaling: rank r holds rows [r*R, (r+1)*R) of one R-MAT table
+    src, dst = rmat_device(spec, device=f"cuda:{local}", start=rank * spec.rows, rows=spec.rows)
     table = gt.edge_table(src, dst)
     edge_spec = gt.EdgeSpec("src", "dst")
     stream = torch.cuda.ExternalStream(_native.stream_handle(), device=dev)
     iters = args.iterations
     state = {}
 
-    def step():
-        g = gt.table_to_graph(table, edge_spec)
-        out = state.get("scores")
-        if out is None or out.shape[0] != g.node_count:
-            out = state["scores"] = torch.empty(g.node_count, dtype=torch.float64, device=dev)
-        gt.pagerank_device(g, 0.85, iters, out.data_ptr())
-        tc = gt.triangle_count(g)
-        state.update(n=g.node_count, e=g.edge_count, tc=tc)
-        del g
+    sharded = world > 1 or args.sharded
+    if sharded and not dist_ready():
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    if not sharded:
+        def step():
+            g = gt.table_to_graph(table, edge_spec)
+            out = state.get("scores")
+            if out is None or out.shape[0] != g.node_count:
+                out = state["scores"] = torch.empty(g.node_count, dtype=torch.float64, device=dev)
+            gt.pagerank_device(g, 0.85, iters, out.data_ptr())
+            tc = gt.triangle_count(g)
+            state.update(n=g.node_count, e=g.edge_count, tc=tc)
+            del g
+    else:
+        from paper_1503_07881_b200 import distributed as D
+
+        ops = D.NativeOps(dev)
+
+        def step():
+            sg = D.build_csr(src, dst, ops=ops)
+            D.pagerank(sg, 0.85, iters, ops=ops)
+            tc = D.triangle_count(sg, ops=ops)
+            state.update(n=sg.n, e=sg.e, tc=tc)
+            del sg
 
     for _ in range(args.warmup):
         step()
@@ -280,7 +308,7 @@ def ours_arm(args):
         by = sum(v[2] for k, v in phases.items() if k.startswith(prefixes)) / args.steps
         return ms, by
 
-    b_ms, b_bytes = group(("build.", "sort.digit"))
+    b_ms, b_bytes = group(("build.", "sort.", "dist."))
     p_ms, p_bytes = group(("pr.",))
     t_ms, t_bytes = group(("tc.",))
     phase_line = {
@@ -322,11 +350,20 @@ def ours_arm(args):
         state.clear()
         torch.cuda.empty_cache()
 
-        def e2e_step():
-            g = gt.table_to_graph(host_table, edge_spec)
-            pr = gt.pagerank(g, 0.85, iters)
-            tc_ = gt.triangle_count(g)
-            return pr, tc_
+        if not sharded:
+            def e2e_step():
+                g = gt.table_to_graph(host_table, edge_spec)
+                pr = gt.pagerank(g, 0.85, iters)
+                tc_ = gt.triangle_count(g)
+                return pr, tc_
+        else:
+            def e2e_step():
+                s_d = h_src.to(dev, non_blocking=True)
+                d_d = h_dst.to(dev, non_blocking=True)
+                sg = D.build_csr(s_d, d_d, ops=ops)
+                pr = D.pagerank(sg, 0.85, iters, ops=ops).cpu()
+                tc_ = D.triangle_count(sg, ops=ops)
+                return pr, tc_
 
         for _ in range(max(1, min(args.warmup, 2))):
             e2e_step()
@@ -371,12 +408,13 @@ def ours_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int64+f64", "data": "synthetic (R-MAT generated on device, seeded)",
-        "config": {"workload": f"{args.config}: R-MAT s{spec.scale} {rows} rows seed {spec.seed}"
+        "config": {"workload": f"{args.config}: R-MAT s{spec.scale} {rows * world} rows seed {spec.seed}"
                                f" permuted={spec.permute}; ToGraph + PageRank x{iters} fp64 + "
                                "triangles (C3)",
                    "rows": rows, "nodes": n, "edges": e, "triangles": tc,
                    "pagerank_iterations": iters,
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "parallelism": f"sharded x{world} (NCCL)" if sharded else "single",
+                   "rows_per_gpu": rows,
                    "l2": "inputs larger than L2 (16*rows bytes >> 126 MB)"},
         "phases": phase_line, "kernels": kernels, "roofline": roofline,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
@@ -384,7 +422,7 @@ def ours_arm(args):
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_ready():
         import torch.distributed as dist
 
         dist.destroy_process_group()

@@ -142,6 +142,72 @@ GT_API int gt_triangle_orientation(const gt_graph* g, int32_t* h_deg, int32_t* h
 GT_API int gt_rmat_generate(int scale, int64_t rows, double a, double b, double c,
                      uint64_t seed, int permute, int64_t* d_src, int64_t* d_dst);
 
+/* Rows [start, start+rows) of the same R-MAT table (multi-GPU shards). */
+GT_API int gt_rmat_generate_range(int scale, int64_t start, int64_t rows, double a, double b,
+                                  double c, uint64_t seed, int permute, int64_t* d_src,
+                                  int64_t* d_dst);
+
+/* ---- multi-GPU primitives ------------------------------------------------
+ * One process per GPU; paper_1503_07881_b200/distributed.py runs the
+ * collectives (torch.distributed / NCCL) between these calls. They are the
+ * pieces of gt_build_csr / gt_pagerank / gt_triangles restricted to one
+ * rank's shard; all pointers are device pointers, every call synchronises. */
+
+/* d_out2[0] = min, d_out2[1] = max over the ids of both columns. */
+GT_API int gt_id_minmax(const int64_t* d_src, const int64_t* d_dst, int64_t rows,
+                        int64_t* d_out2);
+/* d_flags[x - lo] = 1 for every id x of both columns (flags zeroed first). */
+GT_API int gt_id_presence(const int64_t* d_src, const int64_t* d_dst, int64_t rows, int64_t lo,
+                          int64_t span, uint8_t* d_flags);
+/* Presence flags (OR over ranks) -> rank map words (uint2[ceil(span/32)]:
+ * 32 presence bits + popcount prefix) and the node count. */
+GT_API int gt_id_rankmap(const uint8_t* d_flags, int64_t span, void* d_words, int64_t* n_nodes);
+/* Sorted distinct ids (N) from the rank map words. */
+GT_API int gt_id_list(const void* d_words, int64_t span, int64_t lo, int64_t* d_ids);
+/* keys[i] = rank(src[i]) << kbits | rank(dst[i]) through the rank map. */
+GT_API int gt_pack_keys(const int64_t* d_src, const int64_t* d_dst, int64_t rows, int64_t lo,
+                        const void* d_words, int kbits, uint64_t* d_keys);
+/* LSD radix sort of n keys on bits [lo_bit, hi_bit); the result is in d_keys
+ * (*result_in_tmp = 0) or d_tmp (1). Stable. */
+GT_API int gt_sort_keys(uint64_t* d_keys, uint64_t* d_tmp, int64_t n, int lo_bit, int hi_bit,
+                        int* result_in_tmp);
+/* Drop adjacent duplicates of sorted keys (convert.py:76-80); *m = kept. */
+GT_API int gt_unique_keys(const uint64_t* d_in, int64_t n, uint64_t* d_out, int64_t* m);
+/* d_counts[b] = #{i : min(keys[i] >> shift, nbuckets-1) == b}, nbuckets <= 4096. */
+GT_API int gt_key_bucket_counts(const uint64_t* d_keys, int64_t n, int shift, int nbuckets,
+                                int64_t* d_counts);
+/* h_out[j] = lower bound of h_bounds[j] in sorted keys (nb <= 4096). */
+GT_API int gt_key_lower_bounds(const uint64_t* d_sorted, int64_t n, const uint64_t* h_bounds,
+                               int nb, int64_t* h_out);
+/* (a << kbits | b) -> (b << kbits | a). */
+GT_API int gt_swap_key_halves(const uint64_t* d_in, int64_t n, int kbits, uint64_t* d_out);
+/* Sorted keys of rows [row_lo, row_lo+rows) -> d_off[rows+1] (local, from 0),
+ * d_adj[m] (low kbits). d_tmp: scratch of m keys (used when row_lo != 0). */
+GT_API int gt_csr_from_keys(const uint64_t* d_sorted, int64_t m, int kbits, int64_t row_lo,
+                            int64_t rows, uint64_t* d_tmp, int64_t* d_off, int32_t* d_adj);
+/* A gt_graph from full device CSR arrays (copied), e.g. replicated shards. */
+GT_API int gt_graph_from_csr(int64_t n, int64_t e, const int64_t* d_ids, const int64_t* d_out_off,
+                             const int32_t* d_out_adj, const int64_t* d_in_off,
+                             const int32_t* d_in_adj, gt_graph** out);
+/* d_inv[v] = 1/(off[v+1]-off[v]), 0 for an empty row. */
+GT_API int gt_inv_degree(const int64_t* d_off, int64_t rows, double* d_inv);
+/* PageRank start from the full 1/outdeg vector: contrib = inv/N and the
+ * dangling mass (algorithms.py:67-75). */
+GT_API int gt_pagerank_init(const double* d_inv, int64_t n, double* d_contrib,
+                            double* d_dangling);
+/* One PageRank iteration over a dst-row range of the in-CSR (local offsets,
+ * global source indices into the replicated contrib vector): scores of the
+ * rows (last = 1) or their next contributions (last = 0), and the local
+ * dangling partial (algorithms.py:72-85). */
+GT_API int gt_pagerank_step(const int64_t* d_in_off, const int32_t* d_in_adj, int64_t rows,
+                            int64_t e_local, int64_t n_total, const double* d_contrib,
+                            const double* d_inv_rows, const double* d_dangling_prev,
+                            double damping, int last, double* d_score_rows,
+                            double* d_contrib_rows, double* d_dangling_out);
+/* Triangle count restricted to every nparts-th work item starting at part:
+ * the parts of all ranks sum to gt_triangles (the all-reduce is the caller's). */
+GT_API int gt_triangles_part(const gt_graph* g, int part, int nparts, int64_t* count);
+
 /* ---- instrumentation ---------------------------------------------------- */
 
 /* Number of kernels this library has launched since load. */

@@ -44,6 +44,33 @@ SIGNATURES = {
     "gt_rmat_generate": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
                                         ctypes.c_int, _VP, _VP]),
+    "gt_rmat_generate_range": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                              ctypes.c_uint64, ctypes.c_int, _VP, _VP]),
+    "gt_id_minmax": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, _VP]),
+    "gt_id_presence": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                      _VP]),
+    "gt_id_rankmap": (ctypes.c_int, [_VP, ctypes.c_int64, _VP, _I64P]),
+    "gt_id_list": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int64, _VP]),
+    "gt_pack_keys": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_int64, _VP, ctypes.c_int,
+                                    _VP]),
+    "gt_sort_keys": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(ctypes.c_int)]),
+    "gt_unique_keys": (ctypes.c_int, [_VP, ctypes.c_int64, _VP, _I64P]),
+    "gt_key_bucket_counts": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                            _VP]),
+    "gt_key_lower_bounds": (ctypes.c_int, [_VP, ctypes.c_int64, _VP, ctypes.c_int, _VP]),
+    "gt_swap_key_halves": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int, _VP]),
+    "gt_csr_from_keys": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int, ctypes.c_int64,
+                                        ctypes.c_int64, _VP, _VP, _VP]),
+    "gt_graph_from_csr": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, _VP, _VP, _VP, _VP, _VP,
+                                         ctypes.POINTER(_VP)]),
+    "gt_inv_degree": (ctypes.c_int, [_VP, ctypes.c_int64, _VP]),
+    "gt_pagerank_init": (ctypes.c_int, [_VP, ctypes.c_int64, _VP, _VP]),
+    "gt_pagerank_step": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                        _VP, _VP, _VP, ctypes.c_double, ctypes.c_int, _VP, _VP,
+                                        _VP]),
+    "gt_triangles_part": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, _I64P]),
     "gt_launch_count": (ctypes.c_int64, []),
     "gt_profile_enable": (ctypes.c_int, [ctypes.c_int]),
     "gt_profile_reset": (ctypes.c_int, []),
@@ -201,11 +228,11 @@ def triangle_orientation(handle: int, n: int):
     return deg, rank, off_p, adj_p
 
 
-def rmat_generate(scale, rows, a, b, c, seed, permute, src_ptr, dst_ptr):
+def rmat_generate(scale, rows, a, b, c, seed, permute, src_ptr, dst_ptr, start=0):
     lib = ensure_init()
-    check(lib.gt_rmat_generate(int(scale), int(rows), float(a), float(b), float(c),
-                               int(seed) & ((1 << 64) - 1), int(bool(permute)), int(src_ptr),
-                               int(dst_ptr)), "gt_rmat_generate")
+    check(lib.gt_rmat_generate_range(int(scale), int(start), int(rows), float(a), float(b),
+                                     float(c), int(seed) & ((1 << 64) - 1), int(bool(permute)),
+                                     int(src_ptr), int(dst_ptr)), "gt_rmat_generate_range")
 
 
 def stream_handle() -> int:

@@ -541,3 +541,289 @@ void gt_graph_free(gt_graph* g) {
 }
 
 }  // extern "C"
+
+// ============================================================================
+// Primitives of the multi-GPU build (paper_1503_07881_b200/distributed.py).
+// One process per GPU; the host-side orchestration exchanges data with
+// torch.distributed (NCCL) between these calls. All pointers are device
+// pointers on the calling process's GPU; every call is stream-synchronous.
+// ============================================================================
+namespace gtd {
+
+__global__ void __launch_bounds__(256) presence_flags_kernel(const int64_t* __restrict__ src,
+                                                             const int64_t* __restrict__ dst,
+                                                             int64_t n, int64_t lo,
+                                                             uint8_t* __restrict__ flags) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    flags[ld_stream_s64(src + i) - lo] = 1;
+    flags[ld_stream_s64(dst + i) - lo] = 1;
+  }
+}
+
+// 32 byte flags -> one presence word (prefix filled by word_prefix_kernel).
+__global__ void __launch_bounds__(256) flags_to_words_kernel(const uint8_t* __restrict__ flags,
+                                                             int64_t span, uint2* __restrict__ words,
+                                                             int64_t nw) {
+  const int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (w >= nw) return;
+  uint32_t bits = 0;
+  const int64_t b0 = w * 32;
+  for (int j = 0; j < 32; ++j)
+    if (b0 + j < span && flags[b0 + j]) bits |= 1u << j;
+  words[w] = make_uint2(bits, 0u);
+}
+
+// keys - (row_lo << kbits): rows become local indices for segment_kernel.
+__global__ void __launch_bounds__(256) rebase_keys_kernel(const uint64_t* __restrict__ in, int64_t n,
+                                                          uint64_t sub, uint64_t* __restrict__ out) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = in[i] - sub;
+}
+
+// (a << k | b) -> (b << k | a)
+__global__ void __launch_bounds__(256) swap_halves_kernel(const uint64_t* __restrict__ in, int64_t n,
+                                                          int kbits, uint64_t* __restrict__ out) {
+  const uint64_t low = (1ull << kbits) - 1ull;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t k = in[i];
+    out[i] = ((k & low) << kbits) | (k >> kbits);
+  }
+}
+
+constexpr int BUCKETS_MAX = 4096;
+__global__ void __launch_bounds__(256) bucket_count_kernel(const uint64_t* __restrict__ keys,
+                                                           int64_t n, int shift, int nb,
+                                                           unsigned long long* __restrict__ out) {
+  __shared__ uint32_t sh[BUCKETS_MAX];
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t b = keys[i] >> shift;
+    atomicAdd(&sh[b < uint64_t(nb) ? b : uint64_t(nb - 1)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb; i += blockDim.x)
+    if (sh[i]) atomicAdd(&out[i], (unsigned long long)sh[i]);
+}
+
+__global__ void lower_bounds_kernel(const uint64_t* __restrict__ keys, int64_t n,
+                                    const uint64_t* __restrict__ bounds, int nb,
+                                    int64_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nb) return;
+  const uint64_t x = bounds[i];
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  out[i] = lo;
+}
+
+}  // namespace gtd
+
+namespace gt {
+
+static int64_t to_host_i64(const int64_t* d) { return read_i64(d); }
+
+}  // namespace gt
+
+extern "C" {
+
+int gt_id_minmax(const int64_t* d_src, const int64_t* d_dst, int64_t rows, int64_t* d_out2) {
+  GT_API_BEGIN
+  require_init();
+  if (rows < 0 || !d_out2) fail(GT_EINVAL, "bad arguments");
+  const long long init[2] = {LLONG_MAX, LLONG_MIN};
+  h2d(d_out2, init, sizeof init);
+  if (rows > 0)
+    GT_LAUNCH(gtd::minmax_kernel, grid_for(rows, 4), 256, 0, d_src, d_dst, rows,
+              reinterpret_cast<long long*>(d_out2));
+  sync();
+  GT_API_END
+}
+
+int gt_id_presence(const int64_t* d_src, const int64_t* d_dst, int64_t rows, int64_t lo,
+                   int64_t span, uint8_t* d_flags) {
+  GT_API_BEGIN
+  require_init();
+  if (rows < 0 || span < 0 || (span > 0 && !d_flags)) fail(GT_EINVAL, "bad arguments");
+  if (span) GT_CUDA(cudaMemsetAsync(d_flags, 0, size_t(span), ctx().stream));
+  if (rows > 0)
+    GT_LAUNCH(gtd::presence_flags_kernel, grid_for(rows, 4), 256, 0, d_src, d_dst, rows, lo,
+              d_flags);
+  sync();
+  GT_API_END
+}
+
+int gt_id_rankmap(const uint8_t* d_flags, int64_t span, void* d_words, int64_t* n_nodes) {
+  GT_API_BEGIN
+  require_init();
+  if (span <= 0 || !d_words || !n_nodes) fail(GT_EINVAL, "bad arguments");
+  const int64_t nw = (span + 31) / 32;
+  uint2* words = static_cast<uint2*>(d_words);
+  GT_LAUNCH(gtd::flags_to_words_kernel, ceil_div(nw, 256), 256, 0, d_flags, span, words, nw);
+  const int64_t tiles = ceil_div64(nw, 256 * 16);
+  uint64_t* status = ws_n<uint64_t>(WS_LOOKBACK, size_t(tiles) + 1);
+  uint32_t* counters = ws_n<uint32_t>(WS_COUNTERS, 64);
+  int64_t* small = ws_n<int64_t>(WS_SMALL, 16);
+  GT_CUDA(cudaMemsetAsync(counters + 16, 0, 4, ctx().stream));
+  GT_LAUNCH(gtd::word_prefix_kernel, static_cast<int>(tiles), 256, 0, words, nw, status,
+            counters + 16, next_epoch(), small + 2);
+  *n_nodes = to_host_i64(small + 2);
+  GT_API_END
+}
+
+int gt_id_list(const void* d_words, int64_t span, int64_t lo, int64_t* d_ids) {
+  GT_API_BEGIN
+  require_init();
+  const int64_t nw = (span + 31) / 32;
+  if (nw > 0)
+    GT_LAUNCH(gtd::ids_kernel, ceil_div(nw, 256), 256, 0, static_cast<const uint2*>(d_words), nw,
+              lo, d_ids);
+  sync();
+  GT_API_END
+}
+
+int gt_pack_keys(const int64_t* d_src, const int64_t* d_dst, int64_t rows, int64_t lo,
+                 const void* d_words, int kbits, uint64_t* d_keys) {
+  GT_API_BEGIN
+  require_init();
+  if (kbits < 1 || kbits > 31) fail(GT_EINVAL, "kbits must be in [1, 31]");
+  if (rows > 0)
+    GT_LAUNCH(gtd::pack_kernel<true>, grid_for(rows, 4), 256, 0, d_src, d_dst, rows, lo,
+              static_cast<const uint2*>(d_words), (const int64_t*)nullptr, int64_t(0), kbits,
+              SortPlan(), (unsigned long long*)nullptr, d_keys);
+  sync();
+  GT_API_END
+}
+
+int gt_sort_keys(uint64_t* d_keys, uint64_t* d_tmp, int64_t n, int lo_bit, int hi_bit,
+                 int* result_in_tmp) {
+  GT_API_BEGIN
+  require_init();
+  if (!result_in_tmp || lo_bit < 0 || hi_bit > 64 || lo_bit > hi_bit) fail(GT_EINVAL, "bad arguments");
+  SortPlan plan = make_plan(lo_bit, hi_bit);
+  SortHist h = sort_hist_begin(0);
+  sort_histogram(d_keys, n, plan, h);
+  uint64_t* out = radix_sort(d_keys, d_tmp, n, plan, h, "dist.sort");
+  *result_in_tmp = out == d_tmp ? 1 : 0;
+  sync();
+  GT_API_END
+}
+
+int gt_unique_keys(const uint64_t* d_in, int64_t n, uint64_t* d_out, int64_t* m) {
+  GT_API_BEGIN
+  require_init();
+  if (!m) fail(GT_EINVAL, "m must not be NULL");
+  *m = 0;
+  if (n > 0) {
+    const int64_t tiles = ceil_div64(n, gtd::SEG_TILE);
+    uint64_t* status = ws_n<uint64_t>(WS_LOOKBACK, size_t(tiles) + 1);
+    uint32_t* counters = ws_n<uint32_t>(WS_COUNTERS, 64);
+    int64_t* small = ws_n<int64_t>(WS_SMALL, 16);
+    GT_CUDA(cudaMemsetAsync(counters + 17, 0, 4, ctx().stream));
+    GT_LAUNCH(gtd::unique_kernel, static_cast<int>(tiles), 256, 0, d_in, n, int64_t(0),
+              reinterpret_cast<int64_t*>(d_out), status, counters + 17, next_epoch(), small + 3);
+    *m = to_host_i64(small + 3);
+  }
+  GT_API_END
+}
+
+int gt_key_bucket_counts(const uint64_t* d_keys, int64_t n, int shift, int nbuckets,
+                         int64_t* d_counts) {
+  GT_API_BEGIN
+  require_init();
+  if (nbuckets < 1 || nbuckets > gtd::BUCKETS_MAX || shift < 0 || shift > 63)
+    fail(GT_EINVAL, "nbuckets must be in [1, 4096]");
+  GT_CUDA(cudaMemsetAsync(d_counts, 0, size_t(nbuckets) * 8, ctx().stream));
+  if (n > 0)
+    GT_LAUNCH(gtd::bucket_count_kernel, grid_for(n, 8), 256, 0, d_keys, n, shift, nbuckets,
+              reinterpret_cast<unsigned long long*>(d_counts));
+  sync();
+  GT_API_END
+}
+
+int gt_key_lower_bounds(const uint64_t* d_sorted, int64_t n, const uint64_t* h_bounds, int nb,
+                        int64_t* h_out) {
+  GT_API_BEGIN
+  require_init();
+  if (nb < 1 || nb > 4096 || !h_bounds || !h_out) fail(GT_EINVAL, "bad arguments");
+  uint64_t* db = reinterpret_cast<uint64_t*>(ws_n<int64_t>(WS_TMP4, size_t(2 * nb)));
+  int64_t* dout = reinterpret_cast<int64_t*>(db + nb);
+  h2d(db, h_bounds, size_t(nb) * 8);
+  GT_LAUNCH(gtd::lower_bounds_kernel, ceil_div(nb, 256), 256, 0, d_sorted, n, db, nb, dout);
+  d2h(h_out, dout, size_t(nb) * 8);
+  sync();
+  GT_API_END
+}
+
+int gt_swap_key_halves(const uint64_t* d_in, int64_t n, int kbits, uint64_t* d_out) {
+  GT_API_BEGIN
+  require_init();
+  if (n > 0) GT_LAUNCH(gtd::swap_halves_kernel, grid_for(n, 4), 256, 0, d_in, n, kbits, d_out);
+  sync();
+  GT_API_END
+}
+
+int gt_csr_from_keys(const uint64_t* d_sorted, int64_t m, int kbits, int64_t row_lo,
+                     int64_t rows, uint64_t* d_tmp, int64_t* d_off, int32_t* d_adj) {
+  GT_API_BEGIN
+  require_init();
+  if (rows < 0 || m < 0 || !d_off) fail(GT_EINVAL, "bad arguments");
+  if (m == 0) {
+    GT_CUDA(cudaMemsetAsync(d_off, 0, size_t(rows + 1) * 8, ctx().stream));
+  } else {
+    const uint64_t* keys = d_sorted;
+    if (row_lo != 0) {
+      GT_LAUNCH(gtd::rebase_keys_kernel, grid_for(m, 4), 256, 0, d_sorted, m,
+                uint64_t(row_lo) << kbits, d_tmp);
+      keys = d_tmp;
+    }
+    GT_LAUNCH(gtd::segment_kernel<false>, ceil_div(m, gtd::SEG_TILE), 256, 0, keys, m, kbits,
+              rows, d_adj, d_off, (uint64_t*)nullptr, SortPlan(), (unsigned long long*)nullptr,
+              (uint64_t*)nullptr, (uint32_t*)nullptr, 0u, (int64_t*)nullptr);
+  }
+  sync();
+  GT_API_END
+}
+
+int gt_graph_from_csr(int64_t n, int64_t e, const int64_t* d_ids, const int64_t* d_out_off,
+                      const int32_t* d_out_adj, const int64_t* d_in_off, const int32_t* d_in_adj,
+                      gt_graph** out) {
+  GT_API_BEGIN
+  require_init();
+  if (!out || n < 0 || e < 0) fail(GT_EINVAL, "bad arguments");
+  *out = nullptr;
+  if (n >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "graph has >= 2^31 nodes");
+  gt_graph* g = new gt_graph();
+  try {
+    cudaStream_t s = ctx().stream;
+    g->n = n;
+    g->e = e;
+    g->kbits = bits_for(n);
+    g->ids = dalloc_n<int64_t>(n);
+    g->out_off = dalloc_n<int64_t>(n + 1);
+    g->in_off = dalloc_n<int64_t>(n + 1);
+    g->out_adj = dalloc_n<int32_t>(e);
+    g->in_adj = dalloc_n<int32_t>(e);
+    GT_CUDA(cudaMemcpyAsync(g->ids, d_ids, size_t(n) * 8, cudaMemcpyDeviceToDevice, s));
+    GT_CUDA(cudaMemcpyAsync(g->out_off, d_out_off, size_t(n + 1) * 8, cudaMemcpyDeviceToDevice, s));
+    GT_CUDA(cudaMemcpyAsync(g->in_off, d_in_off, size_t(n + 1) * 8, cudaMemcpyDeviceToDevice, s));
+    GT_CUDA(cudaMemcpyAsync(g->out_adj, d_out_adj, size_t(e) * 4, cudaMemcpyDeviceToDevice, s));
+    GT_CUDA(cudaMemcpyAsync(g->in_adj, d_in_adj, size_t(e) * 4, cudaMemcpyDeviceToDevice, s));
+    sync();
+  } catch (...) {
+    graph_free(g);
+    throw;
+  }
+  *out = g;
+  GT_API_END
+}
+
+}  // extern "C"

@@ -199,7 +199,8 @@ __device__ __forceinline__ void pr_rows(const double* vals, const PrRows& sr,
       } else {
         const double sc = base + damping * sum;
         const double inv = s < PR_ROWCAP ? sr.inv[s] : inv_out[row];
-        if (!last_iter) contrib_next[s < PR_ROWCAP ? sr.pos[s] : pos[row]] = sc * inv;
+        if (!last_iter)
+          contrib_next[s < PR_ROWCAP ? sr.pos[s] : (pos ? int64_t(pos[row]) : row)] = sc * inv;
         else score[row] = sc;
         if (inv == 0.0) dang += sc;
       }
@@ -209,7 +210,7 @@ __device__ __forceinline__ void pr_rows(const double* vals, const PrRows& sr,
 
 __global__ void __launch_bounds__(PR_THREADS) pr_spmv_kernel(
     const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_adj, int64_t n, int64_t e,
-    const int64_t* __restrict__ tile_row, const double* __restrict__ contrib,
+    int64_t n_total, const int64_t* __restrict__ tile_row, const double* __restrict__ contrib,
     const double* __restrict__ inv_out, const int32_t* __restrict__ pos,
     const double* __restrict__ dangling_prev, double damping,
     double* __restrict__ score, double* __restrict__ contrib_next, double* __restrict__ head,
@@ -223,7 +224,8 @@ __global__ void __launch_bounds__(PR_THREADS) pr_spmv_kernel(
   const int64_t e1 = min(e, e0 + PR_TILE);
   const int ne = e1 > e0 ? int(e1 - e0) : 0;
   const int64_t ra = tile_row[c], rb = tile_row[c + 1];
-  const double base = (1.0 - damping) / double(n) + damping * (*dangling_prev / double(n));
+  const double base =
+      (1.0 - damping) / double(n_total) + damping * (*dangling_prev / double(n_total));
   if (threadIdx.x == 0) tail_row[c] = -1;
   // segments: the head row ra-1 (starts before the tile) when it reaches
   // into it, then rows ra..rb-1 (start inside); the last may run past e1
@@ -248,7 +250,7 @@ __global__ void __launch_bounds__(PR_THREADS) pr_spmv_kernel(
     sr.off[r] = uint16_t(x < 0 ? 0 : (x > ne ? ne : x));
     if (r < nseg && r < PR_ROWCAP) {
       sr.inv[r] = inv_out[row];
-      sr.pos[r] = pos[row];
+      sr.pos[r] = pos ? pos[row] : int32_t(row);
     }
   }
 #pragma unroll
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(PR_THREADS) pr_spmv_kernel(
 }
 
 __global__ void __launch_bounds__(256) pr_fixup_kernel(
-    const int64_t* __restrict__ in_off, int64_t n, int64_t tiles,
+    const int64_t* __restrict__ in_off, int64_t n, int64_t n_total, int64_t tiles,
     const double* __restrict__ inv_out, const int32_t* __restrict__ pos,
     const double* __restrict__ dangling_prev, double damping,
     const double* __restrict__ head, const double* __restrict__ tail,
@@ -285,7 +287,8 @@ __global__ void __launch_bounds__(256) pr_fixup_kernel(
     double* __restrict__ dangling_next) {
   __shared__ double s_red[8];
   const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const double base = (1.0 - damping) / double(n) + damping * (*dangling_prev / double(n));
+  const double base =
+      (1.0 - damping) / double(n_total) + damping * (*dangling_prev / double(n_total));
   double dang = 0.0;
   if (c < tiles) {
     dang = dpart[c];
@@ -297,12 +300,42 @@ __global__ void __launch_bounds__(256) pr_fixup_kernel(
       const double sc = base + damping * sum;
       const double inv = inv_out[v];
       if (last_iter) score[v] = sc;
-      else contrib_next[pos[v]] = sc * inv;
+      else contrib_next[pos ? int64_t(pos[v]) : v] = sc * inv;
       if (inv == 0.0) dang += sc;
     }
   }
   dang = block_sum_256(dang, s_red);
   grid_reduce_last(dang, partials, ticket, dangling_next);
+}
+
+// Distributed PageRank helpers: 1/outdeg of a CSR row range, and the start
+// vector (contrib = inv/N) with its dangling mass, from a full 1/outdeg vector.
+__global__ void __launch_bounds__(256) pr_inv_degree_kernel(const int64_t* __restrict__ off,
+                                                            int64_t rows,
+                                                            double* __restrict__ inv) {
+  const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= rows) return;
+  const int64_t d = off[v + 1] - off[v];
+  inv[v] = d ? 1.0 / double(d) : 0.0;
+}
+
+__global__ void __launch_bounds__(256) pr_init_from_inv_kernel(const double* __restrict__ inv,
+                                                               int64_t n,
+                                                               double* __restrict__ contrib,
+                                                               double* __restrict__ partials,
+                                                               unsigned int* __restrict__ ticket,
+                                                               double* __restrict__ dangling0) {
+  __shared__ double s_red[8];
+  const double s0 = 1.0 / double(n);
+  double dang = 0.0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+    const double iv = inv[v];
+    contrib[v] = s0 * iv;
+    if (iv == 0.0) dang += s0;
+  }
+  dang = block_sum_256(dang, s_red);
+  grid_reduce_last(dang, partials, ticket, dangling0);
 }
 
 }  // namespace gtd
@@ -386,12 +419,12 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
     {
       Phase ph("pr.spmv", 12.0 * e + 8.0 * (n + 1) + 20.0 * n);
       GT_LAUNCH(gtd::pr_spmv_kernel, static_cast<int>(tiles), gtd::PR_THREADS, 0, g->in_off,
-                in_adj_r, n, e, tile_row, cur, inv_out, pos, dang + it, damping, score, nxt, head,
-                tail, tail_row, dpart, last);
+                in_adj_r, n, e, n, tile_row, cur, inv_out, pos, dang + it, damping, score, nxt,
+                head, tail, tail_row, dpart, last);
     }
     {
       Phase ph("pr.fixup", 40.0 * tiles);
-      GT_LAUNCH(gtd::pr_fixup_kernel, fix_blocks, 256, 0, g->in_off, n, tiles, inv_out, pos,
+      GT_LAUNCH(gtd::pr_fixup_kernel, fix_blocks, 256, 0, g->in_off, n, n, tiles, inv_out, pos,
                 dang + it, damping, head, tail, tail_row, dpart, score, nxt, last, partials,
                 ticket, dang + it + 1);
     }
@@ -415,3 +448,87 @@ extern "C" int gt_pagerank(const gt_graph* g, double damping, int iterations, do
   pagerank(g, damping, iterations, scores, scores_is_device != 0);
   GT_API_END
 }
+
+// ============================================================================
+// Primitives of the multi-GPU PageRank (paper_1503_07881_b200/distributed.py):
+// each rank owns a dst-row range of the in-CSR; the contrib vector is
+// replicated (all-gathered every iteration) and the dangling mass all-reduced.
+// ============================================================================
+namespace gt {
+
+static void pr_step_impl(const int64_t* in_off, const int32_t* in_adj, int64_t rows,
+                         int64_t e, int64_t n_total, const double* contrib_full,
+                         const double* inv_rows, const double* dangling_prev, double damping,
+                         int last, double* score_rows, double* contrib_rows, double* dangling_out) {
+  const int64_t tiles = std::max<int64_t>(1, ceil_div64(e, gtd::PR_TILE));
+  const int fix_blocks = ceil_div(tiles, 256);
+  const size_t bytes = size_t(tiles + 1) * 8 * 5 + size_t(fix_blocks) * 8 + 256;
+  char* p = static_cast<char*>(ws_get(WS_TMP1, bytes));
+  auto carve = [&](size_t b) { char* r = p; p += (b + 15) & ~size_t(15); return r; };
+  int64_t* tile_row = reinterpret_cast<int64_t*>(carve(size_t(tiles + 1) * 8));
+  double* head = reinterpret_cast<double*>(carve(size_t(tiles) * 8));
+  double* tail = reinterpret_cast<double*>(carve(size_t(tiles) * 8));
+  int64_t* tail_row = reinterpret_cast<int64_t*>(carve(size_t(tiles) * 8));
+  double* dpart = reinterpret_cast<double*>(carve(size_t(tiles) * 8));
+  double* partials = reinterpret_cast<double*>(carve(size_t(fix_blocks) * 8));
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(carve(16));
+  GT_CUDA(cudaMemsetAsync(ticket, 0, 16, ctx().stream));
+  Phase ph("pr.step", 12.0 * e + 8.0 * (rows + 1) + 24.0 * rows);
+  GT_LAUNCH(gtd::pr_tile_rows_kernel, ceil_div(tiles + 1, 256), 256, 0, in_off, rows, tiles,
+            tile_row);
+  GT_LAUNCH(gtd::pr_spmv_kernel, static_cast<int>(tiles), gtd::PR_THREADS, 0, in_off, in_adj, rows,
+            e, n_total, tile_row, contrib_full, inv_rows, (const int32_t*)nullptr, dangling_prev,
+            damping, score_rows, contrib_rows, head, tail, tail_row, dpart, last);
+  GT_LAUNCH(gtd::pr_fixup_kernel, fix_blocks, 256, 0, in_off, rows, n_total, tiles, inv_rows,
+            (const int32_t*)nullptr, dangling_prev, damping, head, tail, tail_row, dpart,
+            score_rows, contrib_rows, last, partials, ticket, dangling_out);
+}
+
+}  // namespace gt
+
+extern "C" {
+
+int gt_inv_degree(const int64_t* d_off, int64_t rows, double* d_inv) {
+  GT_API_BEGIN
+  require_init();
+  if (rows < 0) fail(GT_EINVAL, "rows must be >= 0");
+  if (rows > 0) GT_LAUNCH(gtd::pr_inv_degree_kernel, ceil_div(rows, 256), 256, 0, d_off, rows, d_inv);
+  sync();
+  GT_API_END
+}
+
+int gt_pagerank_init(const double* d_inv, int64_t n, double* d_contrib, double* d_dangling) {
+  GT_API_BEGIN
+  require_init();
+  if (n < 1) fail(GT_EINVAL, "pagerank needs a non-empty graph");
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div64(n, 256), 4LL * ctx().sm_count));
+  char* p = static_cast<char*>(ws_get(WS_TMP1, size_t(blocks) * 8 + 64));
+  double* partials = reinterpret_cast<double*>(p);
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(p + size_t(blocks) * 8 + 16);
+  GT_CUDA(cudaMemsetAsync(ticket, 0, 16, ctx().stream));
+  GT_LAUNCH(gtd::pr_init_from_inv_kernel, blocks, 256, 0, d_inv, n, d_contrib, partials, ticket,
+            d_dangling);
+  sync();
+  GT_API_END
+}
+
+int gt_pagerank_step(const int64_t* d_in_off, const int32_t* d_in_adj, int64_t rows,
+                     int64_t e_local, int64_t n_total, const double* d_contrib,
+                     const double* d_inv_rows, const double* d_dangling_prev, double damping,
+                     int last, double* d_score_rows, double* d_contrib_rows,
+                     double* d_dangling_out) {
+  GT_API_BEGIN
+  require_init();
+  if (!(damping > 0.0 && damping < 1.0)) fail(GT_EINVAL, "damping must be in (0, 1)");
+  if (rows < 0 || e_local < 0 || n_total < 1) fail(GT_EINVAL, "bad sizes");
+  if (rows == 0) {
+    GT_CUDA(cudaMemsetAsync(d_dangling_out, 0, 8, ctx().stream));
+  } else {
+    pr_step_impl(d_in_off, d_in_adj, rows, e_local, n_total, d_contrib, d_inv_rows,
+                 d_dangling_prev, damping, last, d_score_rows, d_contrib_rows, d_dangling_out);
+  }
+  sync();
+  GT_API_END
+}
+
+}  // extern "C"

@@ -42,13 +42,14 @@ __device__ __forceinline__ uint64_t feistel_perm(uint64_t x, const RmatParams& p
   return x;
 }
 
-__global__ void __launch_bounds__(256) rmat_kernel(int64_t rows, RmatParams p, int permute,
+__global__ void __launch_bounds__(256) rmat_kernel(int64_t start, int64_t rows, RmatParams p,
+                                                   int permute,
                                                    int64_t* __restrict__ src,
                                                    int64_t* __restrict__ dst) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows; e += stride) {
     uint64_t s = 0, d = 0;
-    const uint64_t base = p.key + uint64_t(e) * uint64_t(p.scale);
+    const uint64_t base = p.key + uint64_t(start + e) * uint64_t(p.scale);
     for (int l = 0; l < p.scale; ++l) {
       const uint64_t u = splitmix64(base + uint64_t(l)) >> 11;
       const uint64_t sb = u >= p.tab ? 1ull : 0ull;                  // quadrants c, d
@@ -69,12 +70,13 @@ __global__ void __launch_bounds__(256) rmat_kernel(int64_t rows, RmatParams p, i
 
 using namespace gt;
 
-extern "C" int gt_rmat_generate(int scale, int64_t rows, double a, double b, double c,
-                                uint64_t seed, int permute, int64_t* d_src, int64_t* d_dst) {
+extern "C" int gt_rmat_generate_range(int scale, int64_t start, int64_t rows, double a, double b,
+                                      double c, uint64_t seed, int permute, int64_t* d_src,
+                                      int64_t* d_dst) {
   GT_API_BEGIN
   require_init();
   if (scale < 1 || scale > 40) fail(GT_EINVAL, "scale must be in [1, 40]");
-  if (rows < 0) fail(GT_EINVAL, "rows must be >= 0");
+  if (rows < 0 || start < 0) fail(GT_EINVAL, "rows and start must be >= 0");
   if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0))
     fail(GT_EINVAL, "R-MAT probabilities must be >= 0 and a+b+c <= 1");
   if (rows == 0) return GT_OK;
@@ -91,8 +93,13 @@ extern "C" int gt_rmat_generate(int scale, int64_t rows, double a, double b, dou
   const int grid = static_cast<int>(std::min<int64_t>(ceil_div64(rows, 256), 16LL * ctx().sm_count));
   {
     Phase ph("synth.rmat", 16.0 * rows);
-    GT_LAUNCH(gtd::rmat_kernel, grid, 256, 0, rows, p, permute, d_src, d_dst);
+    GT_LAUNCH(gtd::rmat_kernel, grid, 256, 0, start, rows, p, permute, d_src, d_dst);
   }
   sync();
   GT_API_END
+}
+
+extern "C" int gt_rmat_generate(int scale, int64_t rows, double a, double b, double c,
+                                uint64_t seed, int permute, int64_t* d_src, int64_t* d_dst) {
+  return gt_rmat_generate_range(scale, 0, rows, a, b, c, seed, permute, d_src, d_dst);
 }

@@ -499,7 +499,8 @@ __global__ void __launch_bounds__(256) tc_count_warp_kernel(
     const int64_t* __restrict__ off_p, const int32_t* __restrict__ adj_p,
     const int64_t* __restrict__ off_m, const int2* __restrict__ nm,
     const int2* __restrict__ tasks, int64_t n_bitmap_tasks, int64_t n_tasks, int64_t n,
-    unsigned int* __restrict__ next_task, unsigned long long* __restrict__ total) {
+    int part, int nparts, unsigned int* __restrict__ next_task,
+    unsigned long long* __restrict__ total) {
   extern __shared__ int32_t s_tab[];  // [8][TC_SLOTS]
   __shared__ uint8_t s_start[8][32 * TC_WIN];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -509,13 +510,14 @@ __global__ void __launch_bounds__(256) tc_count_warp_kernel(
   HashProbe hprobe{tab, 31u, 5};
   unsigned long long acc = 0;
   while (true) {
-    unsigned int it = 0;
-    if (lane == 0) it = atomicAdd(next_task, 1u);
-    it = __shfl_sync(0xffffffffu, it, 0);
-    if (int64_t(it) >= n_tasks) break;
+    unsigned int k = 0;
+    if (lane == 0) k = atomicAdd(next_task, 1u);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    const int64_t it = int64_t(k) * nparts + part;  // this part's share: every nparts-th task
+    if (it >= n_tasks) break;
     const int2 task = tasks[it];
     const int v = task.x;
-    const bool use_bm = int64_t(it) < n_bitmap_tasks;
+    const bool use_bm = it < n_bitmap_tasks;
     if (v != cur_v) {
       const int64_t ov = off_p[v];
       const int dv = int(off_p[v + 1] - ov);
@@ -567,7 +569,7 @@ __global__ void __launch_bounds__(256) tc_count_cta_kernel(
     const int64_t* __restrict__ off_p, const int32_t* __restrict__ adj_p,
     const int64_t* __restrict__ off_m, const int2* __restrict__ nm,
     const int2* __restrict__ tasks, int64_t n_tasks, int log_slots, int32_t* __restrict__ gtab,
-    unsigned long long* __restrict__ total) {
+    int part, int nparts, unsigned long long* __restrict__ total) {
   extern __shared__ int32_t s_dyn[];
   __shared__ uint8_t s_start[8][32 * TC_WIN];
   __shared__ unsigned long long s_red[8];
@@ -575,7 +577,8 @@ __global__ void __launch_bounds__(256) tc_count_cta_kernel(
   int32_t* tab = gtab ? gtab + (int64_t(blockIdx.x) << log_slots) : s_dyn;
   const HashProbe probe{tab, (1u << log_slots) - 1u, log_slots};
   unsigned long long acc = 0;
-  for (int64_t it = blockIdx.x; it < n_tasks; it += gridDim.x) {
+  for (int64_t it = int64_t(blockIdx.x) * nparts + part; it < n_tasks;
+       it += int64_t(gridDim.x) * nparts) {
     const int2 task = tasks[it];
     const int v = task.x;
     const int64_t ov = off_p[v];
@@ -718,8 +721,9 @@ void triangle_orientation(const gt_graph* g, int32_t* h_deg, int32_t* h_rank, in
   sync();
 }
 
-int64_t triangles(const gt_graph* g) {
+int64_t triangles(const gt_graph* g, int part, int nparts) {
   require_init();
+  if (nparts < 1 || part < 0 || part >= nparts) fail(GT_EINVAL, "part must be in [0, nparts)");
   if (!g) fail(GT_EINVAL, "null graph");
   const int64_t n = g->n, e = g->e;
   if (n == 0 || e == 0) return 0;
@@ -795,7 +799,7 @@ int64_t triangles(const gt_graph* g) {
     GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_warp_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     GT_LAUNCH(gtd::tc_count_warp_kernel, ctx().sm_count * 3, 256, smem, o.off_p, o.adj_p, off_m,
-              nm, tasks, n_bm, n_bm + n_wt, n, counters + 22, total);
+              nm, tasks, n_bm, n_bm + n_wt, n, part, nparts, counters + 22, total);
   }
   if (n_ct) {
     Phase ph("tc.count_hash", 0.0);
@@ -818,7 +822,7 @@ int64_t triangles(const gt_graph* g) {
       gtab = ws_n<int32_t>(WS_TMP4, size_t(grid) << log_slots);
     }
     GT_LAUNCH(gtd::tc_count_cta_kernel, grid, 256, smem, o.off_p, o.adj_p, off_m, nm,
-              tasks + n_bm + n_wt, n_ct, log_slots, gtab, total);
+              tasks + n_bm + n_wt, n_ct, log_slots, gtab, part, nparts, total);
   }
   int64_t result = 0;
   d2h(&result, total, 8);
@@ -835,7 +839,14 @@ extern "C" {
 int gt_triangles(const gt_graph* g, int64_t* count) {
   GT_API_BEGIN
   if (!count) fail(GT_EINVAL, "count must not be NULL");
-  *count = triangles(g);
+  *count = triangles(g, 0, 1);
+  GT_API_END
+}
+
+int gt_triangles_part(const gt_graph* g, int part, int nparts, int64_t* count) {
+  GT_API_BEGIN
+  if (!count) fail(GT_EINVAL, "count must not be NULL");
+  *count = triangles(g, part, nparts);
   GT_API_END
 }
 

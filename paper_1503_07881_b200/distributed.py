@@ -1,0 +1,419 @@
+"""Multi-GPU hot path: one process per GPU over ``torch.distributed``.
+
+The reference runs on one big-memory host with a thread pool
+(``parallel.py:39-93``); this module shards the same three steps across the
+GPUs of one box, NCCL over NVLink for the exchanges:
+
+* **ToGraph** — every rank holds a slice of the edge table. Node set: global
+  id range (all-reduce MIN/MAX) and presence flags (all-reduce MAX), so every
+  rank derives the same dense ranks (convert.py:45-59). Out-CSR: local sort +
+  dedupe, then a *sample sort by src range* — splitters from an all-reduced
+  histogram of src-rank buckets (the GPU form of ``parallel_sort``'s
+  splitters, parallel.py:52-93) — and one all-to-all shuffle; each rank sorts
+  and dedupes what it received and owns the out-rows of its src range. In-CSR:
+  the owned edges, swapped to (dst, src), take a second shuffle by dst range.
+* **PageRank** — 1D dst-range partition of the in-CSR; the contribution
+  vector is replicated: every iteration all-gathers the owned slices and
+  all-reduces the dangling mass (algorithms.py:72-85).
+* **Triangles** — the CSR shards are all-gathered (replicated CSR), every
+  rank counts an interleaved share of the work items, and the counts are
+  all-reduced (algorithms.py:110-118).
+
+All O(rows) / O(edges) work runs in libgtb200 kernels (``NativeOps``); this
+module only moves buffers and makes the O(ranks) decisions. ``ops`` is a
+parameter so that the CPU tests can drive the same collective logic with
+``gloo`` and a CPU restatement of the primitives (tests/dist_cpu_ops.py);
+the product path always uses ``NativeOps`` and has no CPU fallback.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .errors import CapacityError
+
+SPLIT_BITS = 12  # splitter histogram: 4096 buckets of src (dst) ranks
+MAX_SPAN = 1 << 33  # presence flags of the id range (1 byte per id)
+
+
+def _bits_for(n: int) -> int:
+    b = 1
+    while b < 63 and (1 << b) < n:
+        b += 1
+    return b
+
+
+# --------------------------------------------------------------------- ops --
+
+class NativeOps:
+    """Per-rank primitives in libgtb200.so on this process's GPU."""
+
+    def __init__(self, device=None):
+        from . import _native
+
+        self._n = _native
+        self.lib = _native.ensure_init()
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+
+    # every call below synchronises the library stream before returning; the
+    # torch stream is synchronised first so collectives have landed
+    def _pre(self):
+        torch.cuda.current_stream(self.device).synchronize()
+
+    def _ck(self, rc, what):
+        self._n.check(rc, what)
+
+    def empty(self, n, dtype):
+        return torch.empty(int(n), dtype=dtype, device=self.device)
+
+    def id_minmax(self, src, dst):
+        self._pre()
+        out = self.empty(2, torch.int64)
+        self._ck(self.lib.gt_id_minmax(src.data_ptr(), dst.data_ptr(), src.numel(),
+                                       out.data_ptr()), "gt_id_minmax")
+        return out
+
+    def id_presence(self, src, dst, lo, span):
+        self._pre()
+        flags = self.empty(span, torch.uint8)
+        self._ck(self.lib.gt_id_presence(src.data_ptr(), dst.data_ptr(), src.numel(), lo, span,
+                                         flags.data_ptr()), "gt_id_presence")
+        return flags
+
+    def id_rankmap(self, flags):
+        import ctypes
+
+        self._pre()
+        span = flags.numel()
+        words = self.empty(2 * ((span + 31) // 32), torch.int32)
+        n = ctypes.c_int64()
+        self._ck(self.lib.gt_id_rankmap(flags.data_ptr(), span, words.data_ptr(),
+                                        ctypes.byref(n)), "gt_id_rankmap")
+        return words, int(n.value)
+
+    def id_list(self, words, span, lo, n):
+        self._pre()
+        ids = self.empty(n, torch.int64)
+        self._ck(self.lib.gt_id_list(words.data_ptr(), span, lo, ids.data_ptr()), "gt_id_list")
+        return ids
+
+    def pack_keys(self, src, dst, lo, words, kbits):
+        self._pre()
+        keys = self.empty(src.numel(), torch.int64)
+        self._ck(self.lib.gt_pack_keys(src.data_ptr(), dst.data_ptr(), src.numel(), lo,
+                                       words.data_ptr(), kbits, keys.data_ptr()), "gt_pack_keys")
+        return keys
+
+    def sort_keys(self, keys, lo_bit, hi_bit):
+        import ctypes
+
+        self._pre()
+        keys = keys.contiguous().clone()
+        tmp = torch.empty_like(keys)
+        which = ctypes.c_int()
+        self._ck(self.lib.gt_sort_keys(keys.data_ptr(), tmp.data_ptr(), keys.numel(), lo_bit,
+                                       hi_bit, ctypes.byref(which)), "gt_sort_keys")
+        return tmp if which.value else keys
+
+    def unique_keys(self, keys):
+        import ctypes
+
+        self._pre()
+        out = torch.empty_like(keys)
+        m = ctypes.c_int64()
+        self._ck(self.lib.gt_unique_keys(keys.data_ptr(), keys.numel(), out.data_ptr(),
+                                         ctypes.byref(m)), "gt_unique_keys")
+        return out[: m.value]
+
+    def bucket_counts(self, keys, shift, nbuckets):
+        self._pre()
+        counts = self.empty(nbuckets, torch.int64)
+        self._ck(self.lib.gt_key_bucket_counts(keys.data_ptr(), keys.numel(), shift, nbuckets,
+                                               counts.data_ptr()), "gt_key_bucket_counts")
+        return counts
+
+    def lower_bounds(self, sorted_keys, bounds):
+        self._pre()
+        b = np.ascontiguousarray(np.asarray(bounds, dtype=np.uint64))
+        out = np.empty(b.shape[0], dtype=np.int64)
+        self._ck(self.lib.gt_key_lower_bounds(sorted_keys.data_ptr(), sorted_keys.numel(),
+                                              b.ctypes.data, b.shape[0], out.ctypes.data),
+                 "gt_key_lower_bounds")
+        return out
+
+    def swap_halves(self, keys, kbits):
+        self._pre()
+        out = torch.empty_like(keys)
+        self._ck(self.lib.gt_swap_key_halves(keys.data_ptr(), keys.numel(), kbits,
+                                             out.data_ptr()), "gt_swap_key_halves")
+        return out
+
+    def csr_from_keys(self, keys, kbits, row_lo, rows):
+        self._pre()
+        off = self.empty(rows + 1, torch.int64)
+        adj = self.empty(max(keys.numel(), 1), torch.int32)
+        tmp = torch.empty_like(keys) if row_lo and keys.numel() else keys
+        self._ck(self.lib.gt_csr_from_keys(keys.data_ptr(), keys.numel(), kbits, row_lo, rows,
+                                           tmp.data_ptr(), off.data_ptr(), adj.data_ptr()),
+                 "gt_csr_from_keys")
+        return off, adj[: keys.numel()]
+
+    def graph_from_csr(self, n, e, ids, out_off, out_adj, in_off, in_adj):
+        import ctypes
+
+        from .graph import DeviceGraph
+
+        self._pre()
+        h = ctypes.c_void_p()
+        self._ck(self.lib.gt_graph_from_csr(n, e, ids.data_ptr(), out_off.data_ptr(),
+                                            out_adj.data_ptr(), in_off.data_ptr(),
+                                            in_adj.data_ptr(), ctypes.byref(h)),
+                 "gt_graph_from_csr")
+        return DeviceGraph(h.value)
+
+    def inv_degree(self, off):
+        self._pre()
+        rows = off.numel() - 1
+        inv = self.empty(max(rows, 1), torch.float64)
+        self._ck(self.lib.gt_inv_degree(off.data_ptr(), rows, inv.data_ptr()), "gt_inv_degree")
+        return inv[:rows]
+
+    def pagerank_init(self, inv_full):
+        self._pre()
+        n = inv_full.numel()
+        contrib = self.empty(n, torch.float64)
+        dangling = self.empty(1, torch.float64)
+        self._ck(self.lib.gt_pagerank_init(inv_full.data_ptr(), n, contrib.data_ptr(),
+                                           dangling.data_ptr()), "gt_pagerank_init")
+        return contrib, dangling
+
+    def pagerank_step(self, in_off, in_adj, n_total, contrib, inv_rows, dangling, damping, last):
+        self._pre()
+        rows = in_off.numel() - 1
+        score = self.empty(max(rows, 1), torch.float64)
+        nxt = self.empty(max(rows, 1), torch.float64)
+        part = self.empty(1, torch.float64)
+        self._ck(self.lib.gt_pagerank_step(in_off.data_ptr(), in_adj.data_ptr(), rows,
+                                           in_adj.numel(), n_total, contrib.data_ptr(),
+                                           inv_rows.data_ptr(), dangling.data_ptr(), damping,
+                                           int(last), score.data_ptr(), nxt.data_ptr(),
+                                           part.data_ptr()), "gt_pagerank_step")
+        return (score[:rows] if last else nxt[:rows]), part
+
+    def triangles_part(self, graph, part, nparts):
+        import ctypes
+
+        self._pre()
+        c = ctypes.c_int64()
+        self._ck(self.lib.gt_triangles_part(graph.handle, part, nparts, ctypes.byref(c)),
+                 "gt_triangles_part")
+        return int(c.value)
+
+
+# ----------------------------------------------------------------- helpers --
+
+def _world(group):
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def _all_gather_var(t: torch.Tensor, group) -> list[torch.Tensor]:
+    """All-gather 1-D tensors of different lengths (padded exchange)."""
+    world, _ = _world(group)
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    sizes = [torch.empty_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    mx = max(max(sizes), 1)
+    pad = torch.zeros(mx, dtype=t.dtype, device=t.device)
+    pad[: t.numel()] = t
+    out = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(out, pad, group=group)
+    return [o[:s] for o, s in zip(out, sizes)]
+
+
+def _exchange(send: torch.Tensor, splits: np.ndarray, group) -> torch.Tensor:
+    """all-to-all with uneven splits: part r of `send` goes to rank r."""
+    world, _ = _world(group)
+    send_counts = torch.tensor(np.diff(splits), dtype=torch.int64, device=send.device)
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    rc = [int(x) for x in recv_counts.tolist()]
+    sc = [int(x) for x in send_counts.tolist()]
+    out = torch.empty(sum(rc), dtype=send.dtype, device=send.device)
+    dist.all_to_all_single(out, send.contiguous(), output_split_sizes=rc, input_split_sizes=sc,
+                           group=group)
+    return out
+
+
+def _range_bounds(counts: np.ndarray, world: int, rows: int, bucket_rows: int) -> list[int]:
+    """Row boundaries of `world` ranges balancing the bucketed counts."""
+    cum = np.cumsum(counts)
+    total = int(cum[-1]) if cum.size else 0
+    bounds = [0]
+    for r in range(1, world):
+        target = total * r / world
+        b = int(np.searchsorted(cum, target, side="left")) + 1  # buckets [0, b) go left
+        bounds.append(min(max(b * bucket_rows, bounds[-1]), rows))
+    bounds.append(rows)
+    return bounds
+
+
+def _shuffle_by_rows(keys_sorted, kbits, bounds, ops, group):
+    """Send each key to the rank owning its row (key >> kbits)."""
+    key_bounds = [int(b) << kbits for b in bounds]
+    idx = ops.lower_bounds(keys_sorted, key_bounds)
+    idx[0], idx[-1] = 0, keys_sorted.numel()
+    return _exchange(keys_sorted, idx, group)
+
+
+def _split_plan(n: int, kbits: int):
+    sb = min(SPLIT_BITS, kbits)
+    return sb, 1 << (kbits - sb)  # bucket bits, rows per bucket
+
+
+# ------------------------------------------------------------------- build --
+
+@dataclass
+class ShardedGraph:
+    """This rank's part of the graph; the ranges are identical on every rank."""
+
+    n: int
+    e: int
+    kbits: int
+    ids: torch.Tensor                      # int64 [n], replicated
+    out_bounds: list[int]                  # src-row ranges of the ranks
+    in_bounds: list[int]                   # dst-row ranges of the ranks
+    out_off: torch.Tensor                  # int64 [rows+1], local offsets
+    out_adj: torch.Tensor                  # int32 dense dst
+    in_off: torch.Tensor
+    in_adj: torch.Tensor                   # int32 dense src
+    out_counts: list[int] = field(default_factory=list)
+    in_counts: list[int] = field(default_factory=list)
+
+
+def build_csr(src: torch.Tensor, dst: torch.Tensor, group=None, ops=None) -> ShardedGraph:
+    """Distributed ToGraph over the row slices (src, dst) of all ranks."""
+    ops = ops or NativeOps()
+    world, rank = _world(group)
+    dev = src.device
+    mm = ops.id_minmax(src, dst)
+    lo_t, hi_t = mm[0:1].clone(), mm[1:2].clone()
+    dist.all_reduce(lo_t, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(hi_t, op=dist.ReduceOp.MAX, group=group)
+    lo, hi = int(lo_t.item()), int(hi_t.item())
+    empty64 = torch.zeros(1, dtype=torch.int64, device=dev)
+    if lo > hi:  # no rows anywhere: empty graph (convert.py:142-143)
+        z32 = torch.zeros(0, dtype=torch.int32, device=dev)
+        return ShardedGraph(0, 0, 1, torch.zeros(0, dtype=torch.int64, device=dev),
+                            [0] * (world + 1), [0] * (world + 1), empty64, z32, empty64.clone(),
+                            z32, [0] * world, [0] * world)
+    span = hi - lo + 1
+    if span > MAX_SPAN:
+        raise CapacityError(f"distributed build needs an id range <= 2^33, got {span}")
+    flags = ops.id_presence(src, dst, lo, span)
+    dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
+    words, n = ops.id_rankmap(flags)
+    del flags
+    if n >= (1 << 31):
+        raise CapacityError("graph has >= 2^31 distinct node ids")
+    ids = ops.id_list(words, span, lo, n)
+    kbits = _bits_for(n)
+    sb, bucket_rows = _split_plan(n, kbits)
+
+    # out-CSR: local sort + dedupe, sample sort by src range, sort + dedupe
+    keys = ops.pack_keys(src, dst, lo, words, kbits)
+    del words
+    keys = ops.unique_keys(ops.sort_keys(keys, 0, 2 * kbits))
+    counts = ops.bucket_counts(keys, 2 * kbits - sb, 1 << sb)
+    dist.all_reduce(counts, group=group)
+    out_bounds = _range_bounds(counts.cpu().numpy(), world, n, bucket_rows)
+    mine = _shuffle_by_rows(keys, kbits, out_bounds, ops, group)
+    mine = ops.unique_keys(ops.sort_keys(mine, 0, 2 * kbits))
+    o_lo, o_hi = out_bounds[rank], out_bounds[rank + 1]
+    out_off, out_adj = ops.csr_from_keys(mine, kbits, o_lo, o_hi - o_lo)
+
+    # in-CSR: the owned edges as (dst, src), shuffled by dst range
+    ikeys = ops.sort_keys(ops.swap_halves(mine, kbits), 0, 2 * kbits)
+    del mine
+    counts = ops.bucket_counts(ikeys, 2 * kbits - sb, 1 << sb)
+    dist.all_reduce(counts, group=group)
+    in_bounds = _range_bounds(counts.cpu().numpy(), world, n, bucket_rows)
+    theirs = _shuffle_by_rows(ikeys, kbits, in_bounds, ops, group)
+    del ikeys
+    theirs = ops.sort_keys(theirs, 0, 2 * kbits)
+    i_lo, i_hi = in_bounds[rank], in_bounds[rank + 1]
+    in_off, in_adj = ops.csr_from_keys(theirs, kbits, i_lo, i_hi - i_lo)
+
+    ec = torch.tensor([out_adj.numel(), in_adj.numel()], dtype=torch.int64, device=dev)
+    all_ec = [torch.empty_like(ec) for _ in range(world)]
+    dist.all_gather(all_ec, ec, group=group)
+    out_counts = [int(x[0].item()) for x in all_ec]
+    in_counts = [int(x[1].item()) for x in all_ec]
+    return ShardedGraph(n, sum(out_counts), kbits, ids, out_bounds, in_bounds, out_off, out_adj,
+                        in_off, in_adj, out_counts, in_counts)
+
+
+def gather_csr(sg: ShardedGraph, group=None):
+    """Replicate the full CSR pair on every rank (offsets rebased)."""
+    def full(off, adj, counts):
+        offs = _all_gather_var(off[:-1], group)
+        adjs = _all_gather_var(adj, group)
+        base = np.concatenate([[0], np.cumsum(counts)])
+        parts = [o + int(b) for o, b in zip(offs, base[:-1])]
+        tail = torch.tensor([int(base[-1])], dtype=torch.int64, device=off.device)
+        return torch.cat(parts + [tail]), torch.cat(adjs)
+
+    out_off, out_adj = full(sg.out_off, sg.out_adj, sg.out_counts)
+    in_off, in_adj = full(sg.in_off, sg.in_adj, sg.in_counts)
+    return out_off, out_adj, in_off, in_adj
+
+
+# ---------------------------------------------------------------- PageRank --
+
+def pagerank(sg: ShardedGraph, damping: float = 0.85, iterations: int = 10, group=None,
+             ops=None) -> torch.Tensor:
+    """Scores of all nodes (id order) on every rank (algorithms.py:36-87)."""
+    if not 0.0 < damping < 1.0:
+        raise ValueError(f"damping must be in (0, 1), got {damping}")
+    if iterations < 1:
+        raise ValueError(f"iterations must be >= 1, got {iterations}")
+    if sg.n == 0:
+        raise ValueError("pagerank needs a non-empty graph")
+    ops = ops or NativeOps()
+    _, rank = _world(group)
+    inv_full = torch.cat(_all_gather_var(ops.inv_degree(sg.out_off), group))
+    contrib, dangling = ops.pagerank_init(inv_full)
+    i_lo, i_hi = sg.in_bounds[rank], sg.in_bounds[rank + 1]
+    inv_rows = inv_full[i_lo:i_hi].contiguous()
+    for it in range(iterations):
+        last = it == iterations - 1
+        vals, part = ops.pagerank_step(sg.in_off, sg.in_adj, sg.n, contrib, inv_rows, dangling,
+                                       damping, last)
+        if last:
+            return torch.cat(_all_gather_var(vals, group))
+        dist.all_reduce(part, group=group)
+        dangling = part
+        contrib = torch.cat(_all_gather_var(vals, group))
+    raise AssertionError("unreachable")
+
+
+# --------------------------------------------------------------- triangles --
+
+def triangle_count(sg: ShardedGraph, group=None, ops=None, graph=None) -> int:
+    """Exact triangle count: replicated CSR, interleaved work split, all-reduce."""
+    if sg.n == 0 or sg.e == 0:
+        return 0
+    ops = ops or NativeOps()
+    world, rank = _world(group)
+    if graph is None:
+        out_off, out_adj, in_off, in_adj = gather_csr(sg, group)
+        graph = ops.graph_from_csr(sg.n, sg.e, sg.ids, out_off, out_adj, in_off, in_adj)
+    c = torch.tensor([ops.triangles_part(graph, rank, world)], dtype=torch.int64,
+                     device=sg.ids.device)
+    dist.all_reduce(c, group=group)
+    return int(c.item())

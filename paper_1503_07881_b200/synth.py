@@ -121,16 +121,17 @@ CONFIGS = {
 }
 
 
-def rmat_device(spec: RmatSpec, device: str = "cuda"):
-    """Generate an R-MAT table straight into HBM (torch int64 tensors)."""
+def rmat_device(spec: RmatSpec, device: str = "cuda", start: int = 0, rows: int | None = None):
+    """Generate rows [start, start+rows) of an R-MAT table straight into HBM."""
     import torch
 
     from . import _native
 
-    src = torch.empty(spec.rows, dtype=torch.int64, device=device)
-    dst = torch.empty(spec.rows, dtype=torch.int64, device=device)
-    _native.rmat_generate(spec.scale, spec.rows, spec.a, spec.b, spec.c, spec.seed,
-                          spec.permute, src.data_ptr(), dst.data_ptr())
+    rows = spec.rows if rows is None else rows
+    src = torch.empty(rows, dtype=torch.int64, device=device)
+    dst = torch.empty(rows, dtype=torch.int64, device=device)
+    _native.rmat_generate(spec.scale, rows, spec.a, spec.b, spec.c, spec.seed, spec.permute,
+                          src.data_ptr(), dst.data_ptr(), start=start)
     return src, dst
 
 

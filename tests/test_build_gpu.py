@@ -49,6 +49,18 @@ def test_c1_config_csr_digests():
         assert sha(getattr(h, f)) == str(gold[f"sha_{f}"]), f
 
 
+@pytest.mark.parametrize("scale,start,rows,permute", [(12, 0, 5000, True), (12, 4000, 1000, True),
+                                                     (22, 68_999_000, 1000, True),
+                                                     (26, 1_469_999_000, 1000, True)])
+def test_device_rmat_row_ranges_match_numpy(scale, start, rows, permute):
+    """gt_rmat_generate_range (the shard generator of multi-GPU runs) is the
+    numpy generator's rows [start, start+rows)."""
+    spec = RmatSpec(scale=scale, rows=rows, seed=3, permute=permute)
+    src, dst = rmat_device(spec, start=start, rows=rows)
+    ws, wd = rmat_edges(scale, rows, seed=3, permute=permute, start=start)
+    assert np.array_equal(src.cpu().numpy(), ws) and np.array_equal(dst.cpu().numpy(), wd)
+
+
 def test_duplicates_collapse_and_empty():
     g = build([1, 2, 1], [2, 3, 2])
     assert g.node_count == 3 and g.edge_count == 2 and g.neighbors(1, "out").tolist() == [2]
