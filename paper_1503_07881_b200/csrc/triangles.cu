@@ -81,6 +81,19 @@ __device__ __forceinline__ bool bsearch_in(const int32_t* __restrict__ list, int
   return lo < len && list[lo] == x;
 }
 
+// tile_row[t] = row holding slot t*TC_CAND_TILE (one binary search per tile,
+// all tiles in parallel, so the candidate kernels start without a serial
+// search chain in their prologue); tile_row[tiles] = n - 1.
+__global__ void __launch_bounds__(256) cand_tile_rows_kernel(const int64_t* __restrict__ cat,
+                                                             int64_t n, int64_t slots,
+                                                             int64_t tiles,
+                                                             int64_t* __restrict__ tile_row) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t > tiles) return;
+  const int64_t e = t < tiles ? t * TC_CAND_TILE : slots - 1;
+  tile_row[t] = row_of(cat, 0, n - 1, e);
+}
+
 enum CandMode { CAND_DEG = 0, CAND_ARCS = 1 };
 
 // Edge-parallel pass over the concatenated candidate slots of all rows.
@@ -94,9 +107,10 @@ enum CandMode { CAND_DEG = 0, CAND_ARCS = 1 };
 // before any of them is consumed.
 template <int MODE>
 __global__ void __launch_bounds__(256) cand_kernel(
-    const int64_t* __restrict__ cat, const int64_t* __restrict__ out_off,
-    const int32_t* __restrict__ out_adj, const int32_t* __restrict__ in_adj, int64_t n,
-    int64_t slots, int32_t* __restrict__ deg, const int32_t* __restrict__ rank, int kbits,
+    const int64_t* __restrict__ cat, const int64_t* __restrict__ tile_row,
+    const int64_t* __restrict__ out_off, const int32_t* __restrict__ out_adj,
+    const int32_t* __restrict__ in_adj, int64_t n, int64_t slots, int32_t* __restrict__ deg,
+    const int32_t* __restrict__ rank, int kbits,
     SortPlan plan, unsigned long long* __restrict__ hist, uint64_t* __restrict__ arcs,
     uint64_t* __restrict__ status, uint32_t* __restrict__ counter, uint32_t epoch,
     int64_t* __restrict__ total_out) {
@@ -114,10 +128,8 @@ __global__ void __launch_bounds__(256) cand_kernel(
   if (tid == 0) {
     const uint32_t t = MODE == CAND_ARCS ? atomicAdd(counter, 1u) : blockIdx.x;
     s_tile = t;
-    const int64_t e0 = int64_t(t) * TC_CAND_TILE;
-    const int64_t e1 = min(slots, e0 + TC_CAND_TILE) - 1;
-    s_r[0] = row_of(cat, 0, n - 1, e0);
-    s_r[1] = row_of(cat, s_r[0], n - 1, e1);
+    s_r[0] = tile_row[t];
+    s_r[1] = tile_row[t + 1];  // the row holding the next tile's first slot (or the last slot)
   }
   __syncthreads();
   const int64_t e0 = int64_t(s_tile) * TC_CAND_TILE;
@@ -647,11 +659,15 @@ static Oriented orient(const gt_graph* g) {
   // 1. undirected degrees over the concatenated (out ++ in) rows
   GT_CUDA(cudaMemsetAsync(o.deg, 0, size_t(n) * 4, s));
   GT_CUDA(cudaMemsetAsync(small + 12, 0, 8, s));
+  int64_t* tile_row = ws_n<int64_t>(WS_TMP1, size_t(tiles) + 1);
   {
     Phase ph("tc.und_degree", cand_bytes);
     GT_LAUNCH(gtd::cat_off_kernel, ceil_div(n + 1, 256), 256, 0, g->out_off, g->in_off, n, cat);
-    GT_LAUNCH(gtd::cand_kernel<gtd::CAND_DEG>, static_cast<int>(tiles), 256, 0, cat, g->out_off,
-              g->out_adj, g->in_adj, n, slots, o.deg, (const int32_t*)nullptr, 0, SortPlan(),
+    GT_LAUNCH(gtd::cand_tile_rows_kernel, ceil_div(tiles + 1, 256), 256, 0, cat, n, slots, tiles,
+              tile_row);
+    GT_LAUNCH(gtd::cand_kernel<gtd::CAND_DEG>, static_cast<int>(tiles), 256, 0, cat, tile_row,
+              g->out_off, g->out_adj, g->in_adj, n, slots, o.deg, (const int32_t*)nullptr, 0,
+              SortPlan(),
               (unsigned long long*)nullptr, (uint64_t*)nullptr, (uint64_t*)nullptr,
               (uint32_t*)nullptr, 0u, (int64_t*)nullptr);
     GT_LAUNCH(gtd::max_i32_kernel, grid_cap(ceil_div64(n, 256)), 256, 0, o.deg, n,
@@ -683,7 +699,7 @@ static Oriented orient(const gt_graph* g) {
     Phase ph("tc.orient", cand_bytes + 8.0 * slots);
     uint64_t* status = ws_n<uint64_t>(WS_LOOKBACK, size_t(tiles) + 1);
     GT_CUDA(cudaMemsetAsync(counters + 20, 0, 4, s));
-    GT_LAUNCH(gtd::cand_kernel<gtd::CAND_ARCS>, static_cast<int>(tiles), 256, 0, cat,
+    GT_LAUNCH(gtd::cand_kernel<gtd::CAND_ARCS>, static_cast<int>(tiles), 256, 0, cat, tile_row,
               g->out_off, g->out_adj, g->in_adj, n, slots, o.deg, o.rank, o.kbits, aplan,
               ah.hist, ka, status, counters + 20, next_epoch(), small + 4);
   }
