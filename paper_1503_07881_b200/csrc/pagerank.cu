@@ -157,7 +157,38 @@ struct PrRows {
   int32_t pos[PR_ROWCAP];
 };
 
-template <int G>
+// Row segments of a tile, summed from the gathered values in shared memory:
+// segments shorter than PR_LONG by one thread each (serial, no shuffles),
+// longer ones by a whole warp (strided + butterfly). The order of every sum
+// is fixed, so results are bitwise reproducible.
+constexpr int PR_LONG = 32;
+
+__device__ __forceinline__ void pr_finish(int64_t s, double sum, const PrRows& sr,
+                                          int64_t first_row, int64_t nseg, bool has_head,
+                                          bool has_tail, int64_t c, double base, double damping,
+                                          const double* __restrict__ inv_out,
+                                          const int32_t* __restrict__ pos,
+                                          double* __restrict__ score,
+                                          double* __restrict__ contrib_next,
+                                          double* __restrict__ head, double* __restrict__ tail,
+                                          int64_t* __restrict__ tail_row, bool last_iter,
+                                          double& dang) {
+  const int64_t row = first_row + s;
+  if (has_head && s == 0) {
+    head[c] = sum;
+  } else if (has_tail && s == nseg - 1) {
+    tail[c] = sum;
+    tail_row[c] = row;
+  } else {
+    const double sc = base + damping * sum;
+    const double inv = s < PR_ROWCAP ? sr.inv[s] : inv_out[row];
+    if (!last_iter)
+      contrib_next[s < PR_ROWCAP ? sr.pos[s] : (pos ? int64_t(pos[row]) : row)] = sc * inv;
+    else score[row] = sc;
+    if (inv == 0.0) dang += sc;
+  }
+}
+
 __device__ __forceinline__ void pr_rows(const double* vals, const PrRows& sr,
                                         const int64_t* __restrict__ in_off, int64_t e0, int ne,
                                         int64_t first_row, int64_t nseg, bool has_head,
@@ -168,43 +199,32 @@ __device__ __forceinline__ void pr_rows(const double* vals, const PrRows& sr,
                                         double* __restrict__ head, double* __restrict__ tail,
                                         int64_t* __restrict__ tail_row, bool last_iter,
                                         double& dang) {
-  constexpr int GPW = 32 / G;  // groups per warp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = lane / G, gl = lane % G;
   auto off_at = [&](int64_t r) -> int {
     if (r < PR_ROWCAP + 1) return sr.off[r];
     const int64_t x = in_off[first_row + r] - e0;
     return int(x < 0 ? 0 : (x > ne ? ne : x));
   };
-  for (int64_t s0 = int64_t(warp) * GPW; s0 < nseg; s0 += int64_t(PR_THREADS / 32) * GPW) {
-    const int64_t s = s0 + grp;
-    const bool active = s < nseg;
-    int a = 0, b = 0;
-    if (active) {
-      a = off_at(s);
-      b = off_at(s + 1);
-    }
+  // short segments: thread per segment
+  for (int64_t s = threadIdx.x; s < nseg; s += PR_THREADS) {
+    const int a = off_at(s), b = off_at(s + 1);
+    if (b - a >= PR_LONG) continue;
     double sum = 0.0;
-    for (int j = a + gl; j < b; j += G) sum += vals[j];
-    __syncwarp();
+    for (int j = a; j < b; ++j) sum += vals[j];
+    pr_finish(s, sum, sr, first_row, nseg, has_head, has_tail, c, base, damping, inv_out, pos,
+              score, contrib_next, head, tail, tail_row, last_iter, dang);
+  }
+  // long segments: warp per segment
+  for (int64_t s = warp; s < nseg; s += PR_THREADS / 32) {
+    const int a = off_at(s), b = off_at(s + 1);
+    if (b - a < PR_LONG) continue;  // warp-uniform
+    double sum = 0.0;
+    for (int j = a + lane; j < b; j += 32) sum += vals[j];
 #pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (active && gl == 0) {
-      const int64_t row = first_row + s;
-      if (has_head && s == 0) {
-        head[c] = sum;
-      } else if (has_tail && s == nseg - 1) {
-        tail[c] = sum;
-        tail_row[c] = row;
-      } else {
-        const double sc = base + damping * sum;
-        const double inv = s < PR_ROWCAP ? sr.inv[s] : inv_out[row];
-        if (!last_iter)
-          contrib_next[s < PR_ROWCAP ? sr.pos[s] : (pos ? int64_t(pos[row]) : row)] = sc * inv;
-        else score[row] = sc;
-        if (inv == 0.0) dang += sc;
-      }
-    }
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0)
+      pr_finish(s, sum, sr, first_row, nseg, has_head, has_tail, c, base, damping, inv_out, pos,
+                score, contrib_next, head, tail, tail_row, last_iter, dang);
   }
 }
 
@@ -260,18 +280,10 @@ __global__ void __launch_bounds__(PR_THREADS) pr_spmv_kernel(
   }
   __syncthreads();
 
-  const int64_t avg = nseg > 0 ? int64_t(ne) / nseg : 32;
   const bool last = last_iter != 0;
   double dang = 0.0;
-#define PR_ROWS(G)                                                                            \
-  pr_rows<G>(vals, sr, in_off, e0, ne, first_row, nseg, has_head, has_tail, c, base, damping, \
-             inv_out, pos, score, contrib_next, head, tail, tail_row, last, dang)
-  if (avg >= 24) PR_ROWS(32);
-  else if (avg >= 12) PR_ROWS(16);
-  else if (avg >= 6) PR_ROWS(8);
-  else if (avg >= 3) PR_ROWS(4);
-  else PR_ROWS(2);
-#undef PR_ROWS
+  pr_rows(vals, sr, in_off, e0, ne, first_row, nseg, has_head, has_tail, c, base, damping,
+          inv_out, pos, score, contrib_next, head, tail, tail_row, last, dang);
   dang = block_sum_256(dang, s_red);
   if (threadIdx.x == 0) dpart[c] = dang;
 }
