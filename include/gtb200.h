@@ -204,8 +204,9 @@ GT_API int gt_pagerank_step(const int64_t* d_in_off, const int32_t* d_in_adj, in
                             const double* d_inv_rows, const double* d_dangling_prev,
                             double damping, int last, double* d_score_rows,
                             double* d_contrib_rows, double* d_dangling_out);
-/* Triangle count restricted to every nparts-th work item starting at part:
- * the parts of all ranks sum to gt_triangles (the all-reduce is the caller's). */
+/* Triangle count restricted to the middle vertices v = part (mod nparts) of
+ * the rank-space orientation: the parts of all ranks sum to gt_triangles
+ * (the all-reduce is the caller's). */
 GT_API int gt_triangles_part(const gt_graph* g, int part, int nparts, int64_t* count);
 
 /* ---- instrumentation ---------------------------------------------------- */

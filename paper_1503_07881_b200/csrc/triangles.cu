@@ -8,28 +8,27 @@
 //
 // Device pipeline (everything after step 2 lives in RANK space: node r is the
 // r-th smallest (degree, id), so N+(r) ⊂ (r, n) and hubs sit at the top):
-//   1 cand_kernel<DEG>   edge-parallel over the 2E "candidate slots" out(i) ++
+//   1 cand_degree_kernel edge-parallel over the 2E "candidate slots" out(i) ++
 //                        in(i): a slot is an undirected neighbour unless it is
 //                        a self-loop or an in-slot whose source is also in the
 //                        sorted out-row (binary search) -> undirected degree
 //   2 rank               radix sort of (degree, id) keys -> rank[id]
-//   3 cand_kernel<ARCS>  same slots; every candidate with a higher rank emits
-//                        the arc key rank(i)<<k | rank(j) (stream-compacted,
-//                        + digit histograms of its sort)
-//   4 radix sort + segment   -> oriented CSR N+ (rows and lists by rank)
-//   5 N- (transpose)     keys v<<32 | arc, stable sort on the v bits -> for
-//                        every v the arcs (u,v), in u order, as (first index
-//                        of N+(u) after v, remaining length): the "suffix"
-//   6 count              task = (v, chunk of N-(v)), one warp each. The N+(v)
+//   3 fill_rows          warp per row: the higher-ranked candidates as rank
+//                        values, compacted into a degree-sized slice and
+//                        sorted in place (shuffle / shared-memory bitonic)
+//   4 place_rows         rows moved to their rank-space slot (offsets = scans
+//                        of d+ and deg - d+ in rank order) -> oriented CSR N+;
+//                        every arc (u,v) filed under N-(v) as the suffix of
+//                        N+(u) after v: (first index, remaining length)
+//   5 count              task = (v, chunk of N-(v)), one warp each. The N+(v)
 //                        membership structure is a per-warp shared-memory
 //                        BITMAP over (v, n) when n-1-v <= 2^16 (the top ranks,
 //                        where R-MAT puts nearly all the work: 94% at C3),
 //                        else a per-warp hash table (or per CTA for large
-//                        d+(v)). For every arc (u,v) the
-//                        warp probes the suffix of N+(u) after v — exactly
-//                        the w > v candidates — flattened across 32 lanes so
-//                        reads stay coalesced; each triangle u<v<w is counted
-//                        once, at its middle vertex v.
+//                        d+(v)). For every arc (u,v) the warp probes the
+//                        suffix of N+(u) after v — exactly the w > v
+//                        candidates — with coalesced reads; each triangle
+//                        u<v<w is counted once, at its middle vertex v.
 // Work = sum over u of d+(u)(d+(u)-1)/2 probes. All arithmetic is integer:
 // exact and independent of scheduling.
 #include "graph.cuh"
@@ -38,6 +37,7 @@
 #include "segment.cuh"
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 
@@ -94,39 +94,26 @@ __global__ void __launch_bounds__(256) cand_tile_rows_kernel(const int64_t* __re
   tile_row[t] = row_of(cat, 0, n - 1, e);
 }
 
-enum CandMode { CAND_DEG = 0, CAND_ARCS = 1 };
-
-// Edge-parallel pass over the concatenated candidate slots of all rows.
-//   CAND_DEG:  deg[row] += candidate slots (undirected degree)
-//   CAND_ARCS: candidates j with rank[j] > rank[row] emit rank(row)<<k|rank(j),
-//              stream-compacted in slot order (decoupled look-back) + their
-//              radix digit histograms
+// Edge-parallel pass over the concatenated candidate slots of all rows:
+// deg[row] += candidate slots (the undirected degree, graphs.py:163-167), and
+// one keep bit per slot (keep_bits, 2E bits) for the row-parallel fill.
 // The tile's row offsets are staged in shared memory (cat and out_off; the
 // in-offset is their difference), so the per-slot row search and offset
 // reads stay on chip; the per-slot global loads of all PER slots are issued
 // before any of them is consumed.
-template <int MODE>
-__global__ void __launch_bounds__(256) cand_kernel(
+__global__ void __launch_bounds__(256) cand_degree_kernel(
     const int64_t* __restrict__ cat, const int64_t* __restrict__ tile_row,
     const int64_t* __restrict__ out_off, const int32_t* __restrict__ out_adj,
     const int32_t* __restrict__ in_adj, int64_t n, int64_t slots, int32_t* __restrict__ deg,
-    const int32_t* __restrict__ rank, int kbits,
-    SortPlan plan, unsigned long long* __restrict__ hist, uint64_t* __restrict__ arcs,
-    uint64_t* __restrict__ status, uint32_t* __restrict__ counter, uint32_t epoch,
-    int64_t* __restrict__ total_out) {
+    uint32_t* __restrict__ keep_bits) {
   constexpr int PER = TC_CAND_TILE / 256;
   __shared__ int64_t s_cat[TC_ROWS_CAP];
   __shared__ int64_t s_oo[TC_ROWS_CAP];
-  __shared__ uint32_t sh[MODE == CAND_ARCS ? gt::RS_MAX_PASSES * 256 : 1];
   __shared__ int64_t s_r[2];
   __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_warp[8];
-  __shared__ uint64_t s_excl;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (MODE == CAND_ARCS)
-    for (int i = tid; i < plan.passes * 256; i += 256) sh[i] = 0;
   if (tid == 0) {
-    const uint32_t t = MODE == CAND_ARCS ? atomicAdd(counter, 1u) : blockIdx.x;
+    const uint32_t t = blockIdx.x;
     s_tile = t;
     s_r[0] = tile_row[t];
     s_r[1] = tile_row[t + 1];  // the row holding the next tile's first slot (or the last slot)
@@ -181,61 +168,18 @@ __global__ void __launch_bounds__(256) cand_kernel(
     if (cand[q] && e - cat_at(r) >= no) cand[q] = !bsearch_in(out_adj + oa, no, j[q]);
   }
 
-  if (MODE == CAND_DEG) {
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const bool valid = row[q] >= 0;
-      const unsigned active = __ballot_sync(0xffffffffu, valid);
-      const unsigned kb = __ballot_sync(0xffffffffu, cand[q]);
-      if (valid) {
-        const unsigned peers = __match_any_sync(active, (unsigned long long)row[q]);
-        const int c = __popc(kb & peers);
-        if (lane == __ffs(peers) - 1 && c) atomicAdd(&deg[row[q]], c);
-      }
-    }
-    return;
-  }
-
-  // ---- CAND_ARCS: rank-space arc keys, compaction ranks -------------------
-  uint64_t key[PER];
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
-    key[q] = 0;
-    if (cand[q]) {
-      const int32_t ri = rank[row[q]], rj = rank[j[q]];
-      cand[q] = rj > ri;
-      key[q] = (uint64_t(ri) << kbits) | uint64_t(rj);
+    const bool valid = row[q] >= 0;
+    const unsigned active = __ballot_sync(0xffffffffu, valid);
+    const unsigned kb = __ballot_sync(0xffffffffu, cand[q]);
+    if (lane == 0 && active) keep_bits[(e0 + int64_t(warp) * 32 * PER + q * 32) >> 5] = kb;
+    if (valid) {
+      const unsigned peers = __match_any_sync(active, (unsigned long long)row[q]);
+      const int c = __popc(kb & peers);
+      if (lane == __ffs(peers) - 1 && c) atomicAdd(&deg[row[q]], c);
     }
   }
-  const unsigned lt = lanemask_lt();
-  uint32_t before[PER], run = 0, bits = 0;
-#pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    const unsigned b = __ballot_sync(0xffffffffu, cand[q]);
-    bits |= uint32_t(cand[q]) << q;
-    before[q] = run + __popc(b & lt);
-    run += __popc(b);
-    if (cand[q]) plan_hist_add(sh, plan, key[q]);
-  }
-  if (lane == 0) s_warp[warp] = run;
-  __syncthreads();
-  uint32_t pre = 0, tot = 0;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    const uint32_t a = s_warp[w];
-    if (w < warp) pre += a;
-    tot += a;
-  }
-  if (tid == 0) {
-    s_excl = lookback_single(status, int(s_tile), epoch, tot);
-    if (int64_t(s_tile) == (slots - 1) / TC_CAND_TILE) *total_out = int64_t(s_excl) + tot;
-  }
-  __syncthreads();
-  const int64_t base = int64_t(s_excl) + pre;
-#pragma unroll
-  for (int q = 0; q < PER; ++q)
-    if ((bits >> q) & 1u) arcs[base + before[q]] = key[q];
-  plan_hist_flush(sh, plan, hist);
 }
 
 // ---- rank (algorithms.py:103-106: lexsort by (degree, id)) ------------------
@@ -275,45 +219,275 @@ __global__ void __launch_bounds__(256) max_i32_kernel(const int32_t* __restrict_
   if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
 }
 
-// ---- N-: the transpose of N+ with arc positions ----------------------------
+// ---- rank-space oriented CSR without a global sort ---------------------------
+// fill_rows: warp per id-row i: the candidates of i (out(i) ++ in(i), self and
+// in-slots already in the sorted out-row dropped) of higher rank, as rank
+// values, compacted into the row's slice of `buf` (capacity deg(i), offsets
+// = scan of the undirected degrees) and sorted there (shuffle bitonic up to
+// 32, per-warp shared-memory bitonic up to TC_SORT_WARP); d+(i) recorded.
+// Rows with more than TC_FILL_BIG candidates go to fill_rows_big (CTA per
+// row); rows with more than TC_SORT_WARP survivors to sort_rows_big.
+constexpr int TC_FILL_BIG = 4096;
+constexpr int TC_SORT_WARP = 1024;
+constexpr int TC_SORT_CTA = 16384;
 
-__global__ void __launch_bounds__(256) nminus_keys_kernel(const int32_t* __restrict__ adj_p,
-                                                          int64_t m, SortPlan plan,
-                                                          unsigned long long* __restrict__ hist,
-                                                          uint64_t* __restrict__ keys) {
-  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
-  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
-  __syncthreads();
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t a = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; a < m; a += stride) {
-    const uint64_t k = (uint64_t(uint32_t(adj_p[a])) << 32) | uint64_t(a);
-    keys[a] = k;
-    plan_hist_add(sh, plan, k);
-  }
-  __syncthreads();
-  plan_hist_flush(sh, plan, hist);
-}
-
-// Remaining length of N+(u) after each arc: warp per row.
-__global__ void __launch_bounds__(256) suffix_len_kernel(const int64_t* __restrict__ off_p,
-                                                         int64_t n, int32_t* __restrict__ sl) {
-  const int64_t wg = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+__device__ __forceinline__ int32_t warp_bitonic32(int32_t x) {
   const int lane = threadIdx.x & 31;
-  for (int64_t u = wg; u < n; u += nw) {
-    const int64_t a = off_p[u], b = off_p[u + 1];
-    for (int64_t k = a + lane; k < b; k += 32) sl[k] = int32_t(b - k - 1);
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+      const bool up = (lane & k) == 0;
+      const bool lower = (lane & j) == 0;
+      x = (lower == up) ? min(x, y) : max(x, y);
+    }
+  }
+  return x;
+}
+
+// Bitonic sort of s[0, p) (p a power of two) by the threads [0, nthreads) of
+// the caller group; `sync` is the group barrier.
+template <typename Sync>
+__device__ __forceinline__ void bitonic_smem(int32_t* s, int p, int t0, int nthreads, Sync sync) {
+  for (int k = 2; k <= p; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = t0; t < p / 2; t += nthreads) {
+        const int e = (t / j) * 2 * j + (t % j);
+        const int f = e + j;
+        const bool up = (e & k) == 0;
+        const int32_t a = s[e], b = s[f];
+        if ((a > b) == up) {
+          s[e] = b;
+          s[f] = a;
+        }
+      }
+      sync();
+    }
   }
 }
 
-// N-(v) entries -> (first position after v in N+(u), remaining length).
-__global__ void __launch_bounds__(256) nminus_fill_kernel(const int32_t* __restrict__ arc_of,
-                                                          const int32_t* __restrict__ sl, int64_t m,
-                                                          int2* __restrict__ nm) {
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
-    const int32_t a = arc_of[i];
-    nm[i] = make_int2(a + 1, sl[a]);
+__global__ void __launch_bounds__(256) i32_to_u64_kernel(const int32_t* __restrict__ in, int64_t n,
+                                                         uint64_t* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = uint64_t(uint32_t(in[i]));
+}
+
+__global__ void __launch_bounds__(256) u64_to_i32_kernel(const uint64_t* __restrict__ in, int64_t n,
+                                                         int32_t* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = int32_t(in[i]);
+}
+
+__global__ void __launch_bounds__(256) deg64_kernel(const int32_t* __restrict__ deg, int64_t n,
+                                                    int64_t* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = deg[i];
+}
+
+__device__ __forceinline__ bool slot_kept(const uint32_t* __restrict__ bits, int64_t slot) {
+  return (__ldg(bits + (slot >> 5)) >> (slot & 31)) & 1u;
+}
+
+__global__ void __launch_bounds__(256) fill_rows_kernel(
+    const int64_t* __restrict__ cat, const int64_t* __restrict__ out_off,
+    const int32_t* __restrict__ out_adj, const int64_t* __restrict__ in_off,
+    const int32_t* __restrict__ in_adj, int64_t n, const int32_t* __restrict__ rank,
+    const uint32_t* __restrict__ keep_bits, const int64_t* __restrict__ und_off,
+    int32_t* __restrict__ buf, int32_t* __restrict__ dplus, int32_t* __restrict__ big_fill,
+    int32_t* __restrict__ big_sort, unsigned int* __restrict__ nbig) {
+  __shared__ int32_t s_sort[8][TC_SORT_WARP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  const int64_t nwarps = int64_t(gridDim.x) * 8;
+  for (int64_t i = int64_t(blockIdx.x) * 8 + warp; i < n; i += nwarps) {
+    const int64_t oo = out_off[i], no = out_off[i + 1] - oo;
+    const int64_t io = in_off[i], ni = in_off[i + 1] - io;
+    const int64_t total = no + ni;
+    if (total > TC_FILL_BIG) {
+      if (lane == 0) big_fill[atomicAdd(&nbig[0], 1u)] = int32_t(i);
+      continue;
+    }
+    const int32_t ri = rank[i];
+    const int64_t c = cat[i];
+    int32_t* row = buf + und_off[i];
+    int cnt = 0;
+    for (int64_t k0 = 0; k0 < total; k0 += 128) {  // 4 x 32 candidates in flight
+      int32_t val[4];
+      bool keep[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t k = k0 + 32 * u + lane;
+        keep[u] = k < total && slot_kept(keep_bits, c + k);
+        val[u] = keep[u] ? (k < no ? out_adj[oo + k] : in_adj[io + (k - no)]) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (keep[u]) {
+          val[u] = rank[val[u]];
+          keep[u] = val[u] > ri;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned b = __ballot_sync(0xffffffffu, keep[u]);
+        if (keep[u]) row[cnt + __popc(b & lt)] = val[u];
+        cnt += __popc(b);
+      }
+    }
+    if (lane == 0) dplus[i] = cnt;
+    __syncwarp();
+    if (cnt <= 32) {
+      int32_t x = lane < cnt ? row[lane] : INT_MAX;
+      x = warp_bitonic32(x);
+      if (lane < cnt) row[lane] = x;
+    } else if (cnt <= TC_SORT_WARP) {
+      int p = 64;
+      while (p < cnt) p <<= 1;
+      int32_t* sm = s_sort[warp];
+      for (int t = lane; t < p; t += 32) sm[t] = t < cnt ? row[t] : INT_MAX;
+      __syncwarp();
+      bitonic_smem(sm, p, lane, 32, [] { __syncwarp(); });
+      for (int t = lane; t < cnt; t += 32) row[t] = sm[t];
+    } else if (lane == 0) {
+      big_sort[atomicAdd(&nbig[1], 1u)] = int32_t(i);
+    }
+    __syncwarp();
+  }
+}
+
+// Rows with more than TC_FILL_BIG candidates, in chunks of TC_BIG_CHUNK
+// candidates, one CTA each: pass 1 counts the kept candidates of every chunk,
+// the host turns the counts into per-chunk output offsets, pass 2 writes.
+// chunk = (row, index of the chunk inside the row).
+constexpr int TC_BIG_CHUNK = 2048;
+
+__device__ __forceinline__ bool big_candidate(const int64_t* __restrict__ cat,
+                                              const int64_t* __restrict__ out_off,
+                                              const int32_t* __restrict__ out_adj,
+                                              const int64_t* __restrict__ in_off,
+                                              const int32_t* __restrict__ in_adj,
+                                              const int32_t* __restrict__ rank,
+                                              const uint32_t* __restrict__ keep_bits, int64_t i,
+                                              int64_t k, int32_t ri, int32_t& val) {
+  const int64_t oo = out_off[i], no = out_off[i + 1] - oo;
+  const int64_t total = no + (in_off[i + 1] - in_off[i]);
+  if (k >= total || !slot_kept(keep_bits, cat[i] + k)) return false;
+  val = rank[k < no ? out_adj[oo + k] : in_adj[in_off[i] + (k - no)]];
+  return val > ri;
+}
+
+__global__ void __launch_bounds__(256) fill_big_count_kernel(
+    const int2* __restrict__ chunks, const int64_t* __restrict__ cat,
+    const int64_t* __restrict__ out_off, const int32_t* __restrict__ out_adj,
+    const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_adj,
+    const int32_t* __restrict__ rank, const uint32_t* __restrict__ keep_bits,
+    int64_t* __restrict__ chunk_cnt) {
+  __shared__ uint32_t s_red[8];
+  const int2 ch = chunks[blockIdx.x];
+  const int64_t i = ch.x;
+  const int32_t ri = rank[i];
+  uint32_t cnt = 0;
+  for (int t = threadIdx.x; t < TC_BIG_CHUNK; t += 256) {
+    int32_t val;
+    cnt += big_candidate(cat, out_off, out_adj, in_off, in_adj, rank, keep_bits, i,
+                         int64_t(ch.y) * TC_BIG_CHUNK + t, ri, val) ? 1u : 0u;
+  }
+  cnt = block_sum_256(cnt, s_red);
+  if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = cnt;
+}
+
+__global__ void __launch_bounds__(256) fill_big_write_kernel(
+    const int2* __restrict__ chunks, const int64_t* __restrict__ chunk_off,
+    const int64_t* __restrict__ row_total, const int64_t* __restrict__ cat,
+    const int64_t* __restrict__ out_off, const int32_t* __restrict__ out_adj,
+    const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_adj,
+    const int32_t* __restrict__ rank, const uint32_t* __restrict__ keep_bits,
+    const int64_t* __restrict__ und_off, int32_t* __restrict__ buf,
+    int32_t* __restrict__ dplus) {
+  __shared__ uint32_t s_scan[8];
+  const int2 ch = chunks[blockIdx.x];
+  const int64_t i = ch.x;
+  const int32_t ri = rank[i];
+  int32_t* row = buf + und_off[i] + chunk_off[blockIdx.x];
+  int64_t run = 0;
+  for (int t0 = 0; t0 < TC_BIG_CHUNK; t0 += 256) {
+    int32_t val = 0;
+    const bool keep = big_candidate(cat, out_off, out_adj, in_off, in_adj, rank, keep_bits, i,
+                                    int64_t(ch.y) * TC_BIG_CHUNK + t0 + threadIdx.x, ri, val);
+    uint32_t tot;
+    const uint32_t pre = block_excl_scan_256<uint32_t>(keep ? 1u : 0u, s_scan, tot);
+    if (keep) row[run + pre] = val;
+    run += tot;
+  }
+  if (ch.y == 0 && threadIdx.x == 0) dplus[i] = int32_t(row_total[blockIdx.x]);
+}
+
+// out[r] = a[rows[r]] (+ a[rows[r] + 1] into out[nr + r] when `both`).
+__global__ void gather_rows_kernel(const int32_t* __restrict__ rows, int nr,
+                                   const int64_t* __restrict__ a64, const int32_t* __restrict__ a32,
+                                   int both, int64_t* __restrict__ out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nr) return;
+  const int64_t i = rows[r];
+  out[r] = a64 ? a64[i] : int64_t(a32[i]);
+  if (both) out[nr + r] = a64[i + 1];
+}
+
+// CTA bitonic sort of the rows with 32 < d+ <= TC_SORT_CTA (dynamic smem).
+__global__ void __launch_bounds__(256) sort_rows_big_kernel(const int32_t* __restrict__ rows,
+                                                            const int64_t* __restrict__ und_off,
+                                                            const int32_t* __restrict__ dplus,
+                                                            int32_t* __restrict__ buf) {
+  extern __shared__ int32_t s_dyn[];
+  const int64_t i = rows[blockIdx.x];
+  const int cnt = dplus[i];
+  if (cnt > TC_SORT_CTA) return;  // host falls back to a radix sort
+  int32_t* row = buf + und_off[i];
+  int p = 64;
+  while (p < cnt) p <<= 1;
+  for (int t = threadIdx.x; t < p; t += 256) s_dyn[t] = t < cnt ? row[t] : INT_MAX;
+  __syncthreads();
+  bitonic_smem(s_dyn, p, int(threadIdx.x), 256, [] { __syncthreads(); });
+  for (int t = threadIdx.x; t < cnt; t += 256) row[t] = s_dyn[t];
+}
+
+// Rank-order counts: dp[rank i] = d+(i), dm[rank i] = deg(i) - d+(i).
+__global__ void __launch_bounds__(256) rank_counts_kernel(const int32_t* __restrict__ rank,
+                                                          const int32_t* __restrict__ deg,
+                                                          const int32_t* __restrict__ dplus,
+                                                          int64_t n, int64_t* __restrict__ dp,
+                                                          int64_t* __restrict__ dm) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t r = rank[i];
+  dp[r] = dplus[i];
+  dm[r] = deg[i] - dplus[i];
+}
+
+// Warp per id-row: the sorted row moves to its rank-space slot of adj_p, and
+// every arc (u,v) at position a is filed under N-(v) as (a+1, remaining
+// length of N+(u)); the order inside an N-(v) list is scheduling dependent,
+// the count is not.
+__global__ void __launch_bounds__(256) place_rows_kernel(
+    const int32_t* __restrict__ rank, const int64_t* __restrict__ und_off,
+    const int32_t* __restrict__ dplus, const int32_t* __restrict__ buf, int64_t n,
+    const int64_t* __restrict__ off_p, const int64_t* __restrict__ off_m,
+    int32_t* __restrict__ adj_p, unsigned int* __restrict__ cur, int2* __restrict__ nm) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nwarps = int64_t(gridDim.x) * 8;
+  for (int64_t i = int64_t(blockIdx.x) * 8 + warp; i < n; i += nwarps) {
+    const int cnt = dplus[i];
+    if (cnt == 0) continue;
+    const int32_t* row = buf + und_off[i];
+    const int64_t a0 = off_p[rank[i]];
+    for (int t = lane; t < cnt; t += 32) {
+      const int32_t v = row[t];
+      const int64_t a = a0 + t;
+      adj_p[a] = v;
+      const unsigned slot = atomicAdd(&cur[v], 1u);
+      nm[off_m[v] + slot] = make_int2(int(a + 1), cnt - t - 1);
+    }
   }
 }
 
@@ -322,14 +496,17 @@ __global__ void __launch_bounds__(256) nminus_fill_kernel(const int32_t* __restr
 // 2: CTA hash tasks. A task is (v, chunk of N-(v)); it needs d+(v), d-(v) >= 1.
 __global__ void __launch_bounds__(256) tc_task_count_kernel(const int64_t* __restrict__ off_p,
                                                             const int64_t* __restrict__ off_m,
-                                                            int64_t n, int64_t* __restrict__ c0,
+                                                            int64_t n, int part, int nparts,
+                                                            int64_t* __restrict__ c0,
                                                             int64_t* __restrict__ c1,
                                                             int64_t* __restrict__ c2) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n) return;
   const int64_t dp = off_p[v + 1] - off_p[v];
   const int64_t dm = off_m[v + 1] - off_m[v];
-  const bool live = dp >= 1 && dm >= 1;
+  // a part owns whole N-(v) lists (v = part mod nparts): the order inside a
+  // list is scheduling dependent, so chunks of one list must stay together
+  const bool live = dp >= 1 && dm >= 1 && v % nparts == part;
   const bool bm = n - 1 - v <= TC_BM_BITS;
   c0[v] = (live && bm) ? (dm + TC_CHUNK - 1) / TC_CHUNK : 0;
   c1[v] = (live && !bm && dp <= TC_WARP_MAX) ? (dm + TC_CHUNK - 1) / TC_CHUNK : 0;
@@ -525,7 +702,7 @@ __global__ void __launch_bounds__(256) tc_count_warp_kernel(
     unsigned int k = 0;
     if (lane == 0) k = atomicAdd(next_task, 1u);
     k = __shfl_sync(0xffffffffu, k, 0);
-    const int64_t it = int64_t(k) * nparts + part;  // this part's share: every nparts-th task
+    const int64_t it = int64_t(k);
     if (it >= n_tasks) break;
     const int2 task = tasks[it];
     const int v = task.x;
@@ -589,8 +766,7 @@ __global__ void __launch_bounds__(256) tc_count_cta_kernel(
   int32_t* tab = gtab ? gtab + (int64_t(blockIdx.x) << log_slots) : s_dyn;
   const HashProbe probe{tab, (1u << log_slots) - 1u, log_slots};
   unsigned long long acc = 0;
-  for (int64_t it = int64_t(blockIdx.x) * nparts + part; it < n_tasks;
-       it += int64_t(gridDim.x) * nparts) {
+  for (int64_t it = blockIdx.x; it < n_tasks; it += gridDim.x) {
     const int2 task = tasks[it];
     const int v = task.x;
     const int64_t ov = off_p[v];
@@ -633,25 +809,30 @@ struct Oriented {
   int32_t* rank = nullptr;   // [n] id -> rank
   int64_t* off_p = nullptr;  // [n+1] by rank
   int32_t* adj_p = nullptr;  // [m] ranks, ascending per row
+  int64_t* off_m = nullptr;  // [n+1] by rank
+  int2* nm = nullptr;        // [m] N-(v) entries: (first index after v in N+(u), remaining)
 };
 
 static Oriented orient(const gt_graph* g) {
   const int64_t n = g->n, e = g->e;
   cudaStream_t s = ctx().stream;
   int64_t* small = ws_n<int64_t>(WS_SMALL, 16);
-  uint32_t* counters = ws_n<uint32_t>(WS_COUNTERS, 64);
   const int64_t slots = 2 * e;
   Oriented o;
   o.n = n;
   o.kbits = bits_for(n);
-  // scratch: cat | off_p (n+1 each) | deg[n] | rank[n]
-  const size_t need = size_t(n + 1) * 8 * 2 + size_t(n) * 8 + 64;
+  // scratch (WS_TMP3): cat | und_off | off_p | off_m (n+1 each) | deg | rank | dplus | cur
+  const size_t need = size_t(n + 1) * 8 * 4 + size_t(n) * 16 + 4 * 4096 * 2 + 256;
   char* p = static_cast<char*>(ws_get(WS_TMP3, need));
-  int64_t* cat = reinterpret_cast<int64_t*>(p);
-  o.off_p = cat + (n + 1);
-  o.deg = reinterpret_cast<int32_t*>(o.off_p + (n + 1));
-  o.rank = o.deg + n;
-  o.adj_p = ws_n<int32_t>(WS_TMP2, size_t(e) + 1);  // m <= E
+  auto carve = [&](size_t b) { char* r = p; p += (b + 15) & ~size_t(15); return r; };
+  int64_t* cat = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
+  int64_t* und_off = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
+  o.off_p = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
+  o.off_m = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
+  o.deg = reinterpret_cast<int32_t*>(carve(size_t(n) * 4));
+  o.rank = reinterpret_cast<int32_t*>(carve(size_t(n) * 4));
+  int32_t* dplus = reinterpret_cast<int32_t*>(carve(size_t(n) * 4));
+  unsigned int* cur = reinterpret_cast<unsigned int*>(carve(size_t(n) * 4));
 
   const int64_t tiles = ceil_div64(slots, gtd::TC_CAND_TILE);
   if (tiles >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangles: too many slot tiles");
@@ -660,26 +841,28 @@ static Oriented orient(const gt_graph* g) {
   GT_CUDA(cudaMemsetAsync(o.deg, 0, size_t(n) * 4, s));
   GT_CUDA(cudaMemsetAsync(small + 12, 0, 8, s));
   int64_t* tile_row = ws_n<int64_t>(WS_TMP1, size_t(tiles) + 1);
+  uint32_t* keep_bits = ws_n<uint32_t>(WS_RANKMAP, size_t(tiles) * (gtd::TC_CAND_TILE / 32));
   {
-    Phase ph("tc.und_degree", cand_bytes);
+    Phase ph("tc.und_degree", cand_bytes + slots / 8.0);
     GT_LAUNCH(gtd::cat_off_kernel, ceil_div(n + 1, 256), 256, 0, g->out_off, g->in_off, n, cat);
     GT_LAUNCH(gtd::cand_tile_rows_kernel, ceil_div(tiles + 1, 256), 256, 0, cat, n, slots, tiles,
               tile_row);
-    GT_LAUNCH(gtd::cand_kernel<gtd::CAND_DEG>, static_cast<int>(tiles), 256, 0, cat, tile_row,
-              g->out_off, g->out_adj, g->in_adj, n, slots, o.deg, (const int32_t*)nullptr, 0,
-              SortPlan(),
-              (unsigned long long*)nullptr, (uint64_t*)nullptr, (uint64_t*)nullptr,
-              (uint32_t*)nullptr, 0u, (int64_t*)nullptr);
+    GT_LAUNCH(gtd::cand_degree_kernel, static_cast<int>(tiles), 256, 0, cat, tile_row,
+              g->out_off, g->out_adj, g->in_adj, n, slots, o.deg, keep_bits);
     GT_LAUNCH(gtd::max_i32_kernel, grid_cap(ceil_div64(n, 256)), 256, 0, o.deg, n,
               reinterpret_cast<int*>(small + 12));
+    GT_LAUNCH(gtd::deg64_kernel, ceil_div(n, 256), 256, 0, o.deg, n, und_off);
+    exclusive_scan_i64(und_off, n, small + 13);  // = 2m
   }
-  int max_deg = 0;
-  d2h(&max_deg, small + 12, 4);
+  int64_t hh[2];
+  d2h(hh, small + 12, sizeof hh);
   sync();
-  uint64_t* ka = ws_n<uint64_t>(WS_KEYS_A, size_t(std::max(n, e)));
-  uint64_t* kbuf = ws_n<uint64_t>(WS_KEYS_B, size_t(std::max(n, e)));
+  const int max_deg = int(hh[0] & 0xffffffff);
+  const int64_t two_m = hh[1];
   // 2. rank = position in (degree, id) order
   {
+    uint64_t* ka = ws_n<uint64_t>(WS_KEYS_A, size_t(n));
+    uint64_t* kbuf = ws_n<uint64_t>(WS_KEYS_B, size_t(n));
     SortPlan plan = make_plan(0, o.kbits + bits_for(int64_t(max_deg) + 1));
     SortHist h = sort_hist_begin(0);
     {
@@ -692,31 +875,123 @@ static Oriented orient(const gt_graph* g) {
     GT_LAUNCH(gtd::rank_scatter_kernel, ceil_div(n, 256), 256, 0, sorted, n,
               (uint64_t(1) << o.kbits) - 1, o.rank);
   }
-  // 3. arcs to higher ranks, as rank-space keys
-  SortPlan aplan = make_plan(0, 2 * o.kbits);
-  SortHist ah = sort_hist_begin(0);
+  // 3. higher-ranked neighbours of every id-row, sorted, in a degree-sized slice
+  int32_t* buf = ws_n<int32_t>(WS_TMP2, size_t(std::max<int64_t>(two_m, 1)));
+  int32_t* lists = reinterpret_cast<int32_t*>(ws_get(WS_TMP4, size_t(n) * 8 + 64));
+  int32_t* big_fill = lists;
+  int32_t* big_sort = lists + n;
+  unsigned int* nbig = reinterpret_cast<unsigned int*>(small + 14);
+  GT_CUDA(cudaMemsetAsync(nbig, 0, 8, s));
   {
-    Phase ph("tc.orient", cand_bytes + 8.0 * slots);
-    uint64_t* status = ws_n<uint64_t>(WS_LOOKBACK, size_t(tiles) + 1);
-    GT_CUDA(cudaMemsetAsync(counters + 20, 0, 4, s));
-    GT_LAUNCH(gtd::cand_kernel<gtd::CAND_ARCS>, static_cast<int>(tiles), 256, 0, cat, tile_row,
-              g->out_off, g->out_adj, g->in_adj, n, slots, o.deg, o.rank, o.kbits, aplan,
-              ah.hist, ka, status, counters + 20, next_epoch(), small + 4);
+    Phase ph("tc.orient", 16.0 * (n + 1) * 2 + 4.0 * slots + 8.0 * n + 4.0 * two_m);
+    GT_LAUNCH(gtd::fill_rows_kernel, grid_cap(ceil_div64(n, 8)), 256, 0, cat, g->out_off,
+              g->out_adj, g->in_off, g->in_adj, n, o.rank, keep_bits, und_off, buf, dplus,
+              big_fill, big_sort, nbig);
+  }
+  unsigned int nb[2];
+  d2h(nb, nbig, sizeof nb);
+  sync();
+  if (nb[0]) {  // rows with many candidates: chunked, two passes
+    Phase ph("tc.orient_big", 0.0);
+    std::vector<int32_t> rows(nb[0]);
+    d2h(rows.data(), big_fill, size_t(nb[0]) * 4);
+    sync();
+    std::sort(rows.begin(), rows.end());  // deterministic chunk order
+    h2d(big_fill, rows.data(), rows.size() * 4);
+    int64_t* d_cc = reinterpret_cast<int64_t*>(ws_get(WS_TMP0, rows.size() * 16 + 64));
+    GT_LAUNCH(gtd::gather_rows_kernel, ceil_div(int64_t(rows.size()), 256), 256, 0, big_fill,
+              int(rows.size()), cat, (const int32_t*)nullptr, 1, d_cc);
+    std::vector<int64_t> cc(2 * rows.size());
+    d2h(cc.data(), d_cc, cc.size() * 8);
+    sync();
+    const int64_t* c0 = cc.data();
+    const int64_t* c1 = cc.data() + rows.size();
+    std::vector<int2> chunks;
+    std::vector<size_t> first(rows.size() + 1, 0);
+    for (size_t r = 0; r < rows.size(); ++r) {
+      const int64_t total = c1[r] - c0[r];
+      first[r] = chunks.size();
+      for (int64_t c = 0; c * gtd::TC_BIG_CHUNK < total; ++c)
+        chunks.push_back(make_int2(rows[r], int(c)));
+    }
+    first[rows.size()] = chunks.size();
+    const size_t nc = chunks.size();
+    char* q = static_cast<char*>(ws_get(WS_TMP0, nc * 32 + 256));  // adj_p comes later
+    int2* d_chunks = reinterpret_cast<int2*>(q);
+    int64_t* d_cnt = reinterpret_cast<int64_t*>(d_chunks + nc + 1);
+    int64_t* d_off = d_cnt + nc + 1;
+    int64_t* d_tot = d_off + nc + 1;
+    h2d(d_chunks, chunks.data(), nc * sizeof(int2));
+    GT_LAUNCH(gtd::fill_big_count_kernel, int(nc), 256, 0, d_chunks, cat, g->out_off, g->out_adj,
+              g->in_off, g->in_adj, o.rank, keep_bits, d_cnt);
+    std::vector<int64_t> cnt(nc), off(nc), tot(nc);
+    d2h(cnt.data(), d_cnt, nc * 8);
+    sync();
+    for (size_t r = 0; r < rows.size(); ++r) {
+      int64_t run = 0;
+      for (size_t c = first[r]; c < first[r + 1]; ++c) { off[c] = run; run += cnt[c]; }
+      for (size_t c = first[r]; c < first[r + 1]; ++c) tot[c] = run;
+    }
+    h2d(d_off, off.data(), nc * 8);
+    h2d(d_tot, tot.data(), nc * 8);
+    GT_LAUNCH(gtd::fill_big_write_kernel, int(nc), 256, 0, d_chunks, d_off, d_tot, cat,
+              g->out_off, g->out_adj, g->in_off, g->in_adj, o.rank, keep_bits, und_off, buf,
+              dplus);
+    // sort the big rows too: warp-sized ones by the CTA sort below as well
+    std::vector<int32_t> extra;
+    for (size_t r = 0; r < rows.size(); ++r)
+      if (tot[first[r]] > 1) extra.push_back(rows[r]);
+    if (!extra.empty()) {
+      h2d(big_sort + nb[1], extra.data(), extra.size() * 4);
+      nb[1] += unsigned(extra.size());
+    }
+  }
+  if (nb[1]) {
+    Phase ph("tc.orient_sort", 0.0);
+    const int smem = gtd::TC_SORT_CTA * 4;
+    GT_CUDA(cudaFuncSetAttribute(gtd::sort_rows_big_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    GT_LAUNCH(gtd::sort_rows_big_kernel, int(nb[1]), 256, smem, big_sort, und_off, dplus, buf);
+    // rows beyond the shared-memory sort: LSD radix sort of that row alone
+    const int nr = int(nb[1]);
+    int64_t* d_cd = reinterpret_cast<int64_t*>(ws_get(WS_TMP0, size_t(nr) * 16 + 64));
+    GT_LAUNCH(gtd::gather_rows_kernel, ceil_div(nr, 256), 256, 0, big_sort, nr,
+              (const int64_t*)nullptr, dplus, 0, d_cd);
+    GT_LAUNCH(gtd::gather_rows_kernel, ceil_div(nr, 256), 256, 0, big_sort, nr, und_off,
+              (const int32_t*)nullptr, 0, d_cd + nr);
+    std::vector<int64_t> cd(2 * size_t(nr));
+    d2h(cd.data(), d_cd, cd.size() * 8);
+    sync();
+    for (int r = 0; r < nr; ++r) {
+      const int64_t c = cd[r], off = cd[nr + r];
+      if (c <= gtd::TC_SORT_CTA) continue;
+      uint64_t* ka = ws_n<uint64_t>(WS_KEYS_A, size_t(c));
+      uint64_t* kbuf = ws_n<uint64_t>(WS_KEYS_B, size_t(c));
+      GT_LAUNCH(gtd::i32_to_u64_kernel, ceil_div(c, 256), 256, 0, buf + off, int64_t(c), ka);
+      SortPlan plan = make_plan(0, o.kbits);
+      SortHist h = sort_hist_begin(0);
+      sort_histogram(ka, c, plan, h);
+      uint64_t* srt = radix_sort(ka, kbuf, c, plan, h, "tc.sort");
+      GT_LAUNCH(gtd::u64_to_i32_kernel, ceil_div(c, 256), 256, 0, srt, int64_t(c), buf + off);
+    }
+  }
+  // 4. rank-space offsets of N+ and N-, then rows placed + N- filed
+  {
+    Phase ph("tc.oriented_csr", 8.0 * n + 16.0 * (n + 1) * 2);
+    GT_LAUNCH(gtd::rank_counts_kernel, ceil_div(n, 256), 256, 0, o.rank, o.deg, dplus, n, o.off_p,
+              o.off_m);
+    exclusive_scan_i64(o.off_p, n, small + 4);
+    exclusive_scan_i64(o.off_m, n, small + 5);
   }
   d2h(&o.m, small + 4, 8);
   sync();
-  profile_add_bytes("tc.orient", 8.0 * o.m);
-  // 4. oriented CSR in rank space
-  uint64_t* arcs = radix_sort(ka, kbuf, o.m, aplan, ah, "tc.sort");
+  o.adj_p = ws_n<int32_t>(WS_TMP0, size_t(o.m) + 1);
+  o.nm = reinterpret_cast<int2*>(ws_get(WS_TMP1, size_t(o.m) * 8 + 16));
   {
-    Phase ph("tc.oriented_csr", 12.0 * o.m + 8.0 * n);
-    if (o.m > 0)
-      GT_LAUNCH(gtd::segment_kernel<false>, ceil_div(o.m, gtd::SEG_TILE), 256, 0, arcs, o.m,
-                o.kbits, n, o.adj_p, o.off_p, (uint64_t*)nullptr, SortPlan(),
-                (unsigned long long*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr, 0u,
-                (int64_t*)nullptr);
-    else
-      GT_CUDA(cudaMemsetAsync(o.off_p, 0, size_t(n + 1) * 8, s));
+    Phase ph("tc.oriented_csr", 8.0 * o.m + 4.0 * o.m + 4.0 * o.m + 8.0 * o.m + 8.0 * n);
+    GT_CUDA(cudaMemsetAsync(cur, 0, size_t(n) * 4, s));
+    GT_LAUNCH(gtd::place_rows_kernel, grid_cap(ceil_div64(n, 8)), 256, 0, o.rank, und_off, dplus,
+              buf, n, o.off_p, o.off_m, o.adj_p, cur, o.nm);
   }
   return o;
 }
@@ -751,40 +1026,20 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
   if (m == 0) return 0;
   if (m >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangles: >= 2^31 undirected edges");
 
-  // 5. N-: arcs (u,v) grouped by v (stable: u ascending), as suffixes of N+(u)
-  char* p = static_cast<char*>(ws_get(WS_TMP1, size_t(m) * 8 + size_t(m) * 4 * 2 +
-                                                    size_t(n + 1) * 8 * 4 + 256));
+  int64_t* off_m = o.off_m;
+  const int2* nm = o.nm;
+  // work-list scratch
+  char* p = static_cast<char*>(ws_get(WS_COLS, size_t(n + 1) * 8 * 3 + 64));
   auto carve = [&](size_t b) { char* r = p; p += (b + 15) & ~size_t(15); return r; };
-  int2* nm = reinterpret_cast<int2*>(carve(size_t(m) * 8));
-  int32_t* arc_of = reinterpret_cast<int32_t*>(carve(size_t(m) * 4));
-  int32_t* sl = reinterpret_cast<int32_t*>(carve(size_t(m) * 4));
-  int64_t* off_m = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
   int64_t* t0 = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
   int64_t* t1 = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
   int64_t* t2 = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
-  uint64_t* ka = ws_n<uint64_t>(WS_KEYS_A, size_t(m));
-  uint64_t* kbuf = ws_n<uint64_t>(WS_KEYS_B, size_t(m));
-  {
-    SortPlan plan = make_plan(32, 32 + o.kbits);
-    SortHist h = sort_hist_begin(1);
-    {
-      Phase ph("tc.nminus", 12.0 * m);
-      GT_LAUNCH(gtd::nminus_keys_kernel, grid_cap(ceil_div64(m, 1024)), 256, 0, o.adj_p, m, plan,
-                h.hist, ka);
-    }
-    uint64_t* sorted = radix_sort(ka, kbuf, m, plan, h, "tc.sort");
-    Phase ph("tc.nminus", 12.0 * m + 8.0 * n + 4.0 * m + 8.0 * (n + 1) + 4.0 * m + 12.0 * m);
-    GT_LAUNCH(gtd::segment_kernel<false>, ceil_div(m, gtd::SEG_TILE), 256, 0, sorted, m, 32, n,
-              arc_of, off_m, (uint64_t*)nullptr, SortPlan(), (unsigned long long*)nullptr,
-              (uint64_t*)nullptr, (uint32_t*)nullptr, 0u, (int64_t*)nullptr);
-    GT_LAUNCH(gtd::suffix_len_kernel, grid_cap(ceil_div64(n, 8)), 256, 0, o.off_p, n, sl);
-    GT_LAUNCH(gtd::nminus_fill_kernel, grid_cap(ceil_div64(m, 1024)), 256, 0, arc_of, sl, m, nm);
-  }
   // 6. work lists
   {
     Phase ph("tc.tasks", 8.0 * (n + 1) * 8);
     GT_CUDA(cudaMemsetAsync(small + 7, 0, 8, s));
-    GT_LAUNCH(gtd::tc_task_count_kernel, ceil_div(n, 256), 256, 0, o.off_p, off_m, n, t0, t1, t2);
+    GT_LAUNCH(gtd::tc_task_count_kernel, ceil_div(n, 256), 256, 0, o.off_p, off_m, n, part, nparts,
+              t0, t1, t2);
     exclusive_scan_i64(t0, n, small + 8);
     exclusive_scan_i64(t1, n, small + 9);
     exclusive_scan_i64(t2, n, small + 10);
@@ -796,7 +1051,7 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
   sync();
   const int64_t max_dp = h[0], n_bm = h[1], n_wt = h[2], n_ct = h[3];
   if (n_bm + n_wt + n_ct >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangle work list too long");
-  int2* tasks = ws_n<int2>(WS_TMP0, size_t(n_bm + n_wt + n_ct) + 1);
+  int2* tasks = ws_n<int2>(WS_TMP2, size_t(n_bm + n_wt + n_ct) + 1);  // buf is dead by now
   {
     Phase ph("tc.tasks", 8.0 * (n_bm + n_wt + n_ct));
     if (n_bm) GT_LAUNCH(gtd::tc_task_fill_kernel, ceil_div(n, 256), 256, 0, t0, n, tasks);
