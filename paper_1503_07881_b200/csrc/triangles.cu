@@ -203,9 +203,13 @@ __global__ void __launch_bounds__(256) rank_keys_kernel(const int32_t* __restric
 
 __global__ void __launch_bounds__(256) rank_scatter_kernel(const uint64_t* __restrict__ sorted,
                                                            int64_t n, uint64_t lowmask,
-                                                           int32_t* __restrict__ rank) {
+                                                           int32_t* __restrict__ rank,
+                                                           int32_t* __restrict__ order) {
   const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r < n) rank[sorted[r] & lowmask] = int32_t(r);
+  if (r >= n) return;
+  const int32_t id = int32_t(sorted[r] & lowmask);
+  rank[id] = int32_t(r);
+  order[r] = id;
 }
 
 __global__ void __launch_bounds__(256) max_i32_kernel(const int32_t* __restrict__ x, int64_t n,
@@ -267,6 +271,58 @@ __device__ __forceinline__ void bitonic_smem(int32_t* s, int p, int t0, int nthr
   }
 }
 
+// Stable LSD radix sort (8-bit digits over the low `kbits` bits) of row[0,
+// cnt) by one warp, cnt <= TC_SORT_WARP: ping-pong between the row (global,
+// L1-resident) and a per-warp shared buffer; per pass a shared histogram,
+// its scan, and a rank/scatter in index order (__match_any_sync peers).
+__device__ __forceinline__ void warp_radix_sort(int32_t* row, int cnt, int32_t* sm,
+                                                uint32_t* hist, int kbits) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  int32_t* src = row;
+  int32_t* dst = sm;
+  for (int shift = 0; shift < kbits; shift += 8) {
+#pragma unroll
+    for (int b = lane; b < 256; b += 32) hist[b] = 0u;
+    __syncwarp();
+    for (int k = lane; k < cnt; k += 32) atomicAdd(&hist[(uint32_t(src[k]) >> shift) & 255u], 1u);
+    __syncwarp();
+    uint32_t h[8], tot = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      h[q] = hist[lane * 8 + q];
+      tot += h[q];
+    }
+    uint32_t run = warp_incl_scan(tot) - tot;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      hist[lane * 8 + q] = run;
+      run += h[q];
+    }
+    __syncwarp();
+    for (int k0 = 0; k0 < cnt; k0 += 32) {
+      const int k = k0 + lane;
+      const bool valid = k < cnt;
+      const int32_t x = valid ? src[k] : 0;
+      const uint32_t d = valid ? (uint32_t(x) >> shift) & 255u : 256u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const int leader = 31 - __clz(peers);
+      uint32_t before = 0;
+      if (valid && lane == leader) before = atomicAdd(&hist[d], __popc(peers));
+      before = __shfl_sync(0xffffffffu, before, leader);
+      if (valid) dst[before + __popc(peers & lt)] = x;
+    }
+    __syncwarp();
+    int32_t* t = src;
+    src = dst;
+    dst = t;
+  }
+  if (src != row) {
+    for (int k = lane; k < cnt; k += 32) row[k] = src[k];
+    __syncwarp();
+  }
+}
+
 __global__ void __launch_bounds__(256) i32_to_u64_kernel(const int32_t* __restrict__ in, int64_t n,
                                                          uint64_t* __restrict__ out) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -295,8 +351,9 @@ __global__ void __launch_bounds__(256) fill_rows_kernel(
     const int32_t* __restrict__ in_adj, int64_t n, const int32_t* __restrict__ rank,
     const uint32_t* __restrict__ keep_bits, const int64_t* __restrict__ und_off,
     int32_t* __restrict__ buf, int32_t* __restrict__ dplus, int32_t* __restrict__ big_fill,
-    int32_t* __restrict__ big_sort, unsigned int* __restrict__ nbig) {
+    int32_t* __restrict__ big_sort, unsigned int* __restrict__ nbig, int kbits) {
   __shared__ int32_t s_sort[8][TC_SORT_WARP];
+  __shared__ uint32_t s_hist[8][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
   const int64_t nwarps = int64_t(gridDim.x) * 8;
@@ -342,13 +399,7 @@ __global__ void __launch_bounds__(256) fill_rows_kernel(
       x = warp_bitonic32(x);
       if (lane < cnt) row[lane] = x;
     } else if (cnt <= TC_SORT_WARP) {
-      int p = 64;
-      while (p < cnt) p <<= 1;
-      int32_t* sm = s_sort[warp];
-      for (int t = lane; t < p; t += 32) sm[t] = t < cnt ? row[t] : INT_MAX;
-      __syncwarp();
-      bitonic_smem(sm, p, lane, 32, [] { __syncwarp(); });
-      for (int t = lane; t < cnt; t += 32) row[t] = sm[t];
+      warp_radix_sort(row, cnt, s_sort[warp], s_hist[warp], kbits);
     } else if (lane == 0) {
       big_sort[atomicAdd(&nbig[1], 1u)] = int32_t(i);
     }
@@ -465,22 +516,24 @@ __global__ void __launch_bounds__(256) rank_counts_kernel(const int32_t* __restr
   dm[r] = deg[i] - dplus[i];
 }
 
-// Warp per id-row: the sorted row moves to its rank-space slot of adj_p, and
-// every arc (u,v) at position a is filed under N-(v) as (a+1, remaining
-// length of N+(u)); the order inside an N-(v) list is scheduling dependent,
-// the count is not.
+// Warp per rank-row (ascending, so N-(v) lists come out nearly sorted by u,
+// which keeps the count's suffix reads local): the sorted row moves to its
+// rank-space slot of adj_p, and every arc (u,v) at position a is filed under
+// N-(v) as (a+1, remaining length of N+(u)); the exact order inside an N-(v)
+// list is scheduling dependent, the count is not.
 __global__ void __launch_bounds__(256) place_rows_kernel(
-    const int32_t* __restrict__ rank, const int64_t* __restrict__ und_off,
+    const int32_t* __restrict__ order, const int64_t* __restrict__ und_off,
     const int32_t* __restrict__ dplus, const int32_t* __restrict__ buf, int64_t n,
     const int64_t* __restrict__ off_p, const int64_t* __restrict__ off_m,
     int32_t* __restrict__ adj_p, unsigned int* __restrict__ cur, int2* __restrict__ nm) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nwarps = int64_t(gridDim.x) * 8;
-  for (int64_t i = int64_t(blockIdx.x) * 8 + warp; i < n; i += nwarps) {
+  for (int64_t r = int64_t(blockIdx.x) * 8 + warp; r < n; r += nwarps) {
+    const int64_t i = order[r];
     const int cnt = dplus[i];
     if (cnt == 0) continue;
     const int32_t* row = buf + und_off[i];
-    const int64_t a0 = off_p[rank[i]];
+    const int64_t a0 = off_p[r];
     for (int t = lane; t < cnt; t += 32) {
       const int32_t v = row[t];
       const int64_t a = a0 + t;
@@ -822,7 +875,7 @@ static Oriented orient(const gt_graph* g) {
   o.n = n;
   o.kbits = bits_for(n);
   // scratch (WS_TMP3): cat | und_off | off_p | off_m (n+1 each) | deg | rank | dplus | cur
-  const size_t need = size_t(n + 1) * 8 * 4 + size_t(n) * 16 + 4 * 4096 * 2 + 256;
+  const size_t need = size_t(n + 1) * 8 * 4 + size_t(n) * 20 + 4 * 4096 * 2 + 256;
   char* p = static_cast<char*>(ws_get(WS_TMP3, need));
   auto carve = [&](size_t b) { char* r = p; p += (b + 15) & ~size_t(15); return r; };
   int64_t* cat = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
@@ -833,6 +886,7 @@ static Oriented orient(const gt_graph* g) {
   o.rank = reinterpret_cast<int32_t*>(carve(size_t(n) * 4));
   int32_t* dplus = reinterpret_cast<int32_t*>(carve(size_t(n) * 4));
   unsigned int* cur = reinterpret_cast<unsigned int*>(carve(size_t(n) * 4));
+  int32_t* order = reinterpret_cast<int32_t*>(carve(size_t(n) * 4));
 
   const int64_t tiles = ceil_div64(slots, gtd::TC_CAND_TILE);
   if (tiles >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangles: too many slot tiles");
@@ -873,7 +927,7 @@ static Oriented orient(const gt_graph* g) {
     uint64_t* sorted = radix_sort(ka, kbuf, n, plan, h, "tc.sort");
     Phase ph("tc.rank", 12.0 * n);
     GT_LAUNCH(gtd::rank_scatter_kernel, ceil_div(n, 256), 256, 0, sorted, n,
-              (uint64_t(1) << o.kbits) - 1, o.rank);
+              (uint64_t(1) << o.kbits) - 1, o.rank, order);
   }
   // 3. higher-ranked neighbours of every id-row, sorted, in a degree-sized slice
   int32_t* buf = ws_n<int32_t>(WS_TMP2, size_t(std::max<int64_t>(two_m, 1)));
@@ -886,7 +940,7 @@ static Oriented orient(const gt_graph* g) {
     Phase ph("tc.orient", 16.0 * (n + 1) * 2 + 4.0 * slots + 8.0 * n + 4.0 * two_m);
     GT_LAUNCH(gtd::fill_rows_kernel, grid_cap(ceil_div64(n, 8)), 256, 0, cat, g->out_off,
               g->out_adj, g->in_off, g->in_adj, n, o.rank, keep_bits, und_off, buf, dplus,
-              big_fill, big_sort, nbig);
+              big_fill, big_sort, nbig, o.kbits);
   }
   unsigned int nb[2];
   d2h(nb, nbig, sizeof nb);
@@ -990,7 +1044,7 @@ static Oriented orient(const gt_graph* g) {
   {
     Phase ph("tc.oriented_csr", 8.0 * o.m + 4.0 * o.m + 4.0 * o.m + 8.0 * o.m + 8.0 * n);
     GT_CUDA(cudaMemsetAsync(cur, 0, size_t(n) * 4, s));
-    GT_LAUNCH(gtd::place_rows_kernel, grid_cap(ceil_div64(n, 8)), 256, 0, o.rank, und_off, dplus,
+    GT_LAUNCH(gtd::place_rows_kernel, grid_cap(ceil_div64(n, 8)), 256, 0, order, und_off, dplus,
               buf, n, o.off_p, o.off_m, o.adj_p, cur, o.nm);
   }
   return o;
