@@ -574,15 +574,26 @@ __global__ void __launch_bounds__(256) tc_task_fill_kernel(const int64_t* __rest
   for (int64_t i = a; i < b; ++i) tasks[i] = make_int2(int(v), int(i - a));
 }
 
+// max d+ (out[0]) and the probe count sum_u d+(u)(d+(u)-1)/2 (out[1]): every
+// suffix element the count kernels read, i.e. their algorithmic traffic.
 __global__ void __launch_bounds__(256) max_dplus_kernel(const int64_t* __restrict__ off, int64_t n,
                                                         unsigned long long* __restrict__ out) {
-  unsigned long long mx = 0;
+  unsigned long long mx = 0, pr = 0;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < n; u += stride)
-    mx = max(mx, (unsigned long long)(off[u + 1] - off[u]));
+  for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < n; u += stride) {
+    const unsigned long long d = (unsigned long long)(off[u + 1] - off[u]);
+    mx = max(mx, d);
+    pr += d * (d - (d > 0)) / 2;
+  }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    pr += __shfl_xor_sync(0xffffffffu, pr, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mx) atomicMax(&out[0], mx);
+    if (pr) atomicAdd(&out[1], pr);
+  }
 }
 
 // ---- membership structures of N+(v) ------------------------------------------
@@ -1091,19 +1102,19 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
   // 6. work lists
   {
     Phase ph("tc.tasks", 8.0 * (n + 1) * 8);
-    GT_CUDA(cudaMemsetAsync(small + 7, 0, 8, s));
+    GT_CUDA(cudaMemsetAsync(small + 14, 0, 16, s));
     GT_LAUNCH(gtd::tc_task_count_kernel, ceil_div(n, 256), 256, 0, o.off_p, off_m, n, part, nparts,
               t0, t1, t2);
     exclusive_scan_i64(t0, n, small + 8);
     exclusive_scan_i64(t1, n, small + 9);
     exclusive_scan_i64(t2, n, small + 10);
     GT_LAUNCH(gtd::max_dplus_kernel, grid_cap(ceil_div64(n, 256)), 256, 0, o.off_p, n,
-              reinterpret_cast<unsigned long long*>(small + 7));
+              reinterpret_cast<unsigned long long*>(small + 14));  // [14] max d+, [15] probes
   }
-  int64_t h[4];
-  d2h(h, small + 7, sizeof h);  // max d+, bitmap / warp / CTA task counts
+  int64_t h[8];
+  d2h(h, small + 8, sizeof h);  // bitmap / warp / CTA task counts, ..., max d+, probes
   sync();
-  const int64_t max_dp = h[0], n_bm = h[1], n_wt = h[2], n_ct = h[3];
+  const int64_t n_bm = h[0], n_wt = h[1], n_ct = h[2], max_dp = h[6], probes = h[7];
   if (n_bm + n_wt + n_ct >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangle work list too long");
   int2* tasks = ws_n<int2>(WS_TMP2, size_t(n_bm + n_wt + n_ct) + 1);  // buf is dead by now
   {
@@ -1115,10 +1126,10 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
   }
   unsigned long long* total = reinterpret_cast<unsigned long long*>(small + 6);
   GT_CUDA(cudaMemsetAsync(total, 0, 8, s));
-  // algorithmic bytes credited: every N- entry and N+ list once (the probed
-  // suffix elements depend on the graph and are not counted)
   if (n_bm + n_wt) {
-    Phase ph("tc.count", 8.0 * m + 4.0 * m);
+    // algorithmic bytes: every probed suffix element (4 B), the N- entries (8 B)
+    // and the N+ lists loaded into tables (4 B); hash tasks counted here too
+    Phase ph("tc.count", 4.0 * double(probes) + 12.0 * m);
     GT_CUDA(cudaMemsetAsync(counters + 22, 0, 4, s));
     const int smem = 8 * gtd::TC_SLOTS * 4;
     GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_warp_kernel,
