@@ -168,16 +168,23 @@ __global__ void __launch_bounds__(256) cand_degree_kernel(
     if (cand[q] && e - cat_at(r) >= no) cand[q] = !bsearch_in(out_adj + oa, no, j[q]);
   }
 
+  // per-row counts: the 32 slots of a warp step are consecutive, so each row
+  // is a run of lanes; the first lane of a run adds the run's kept count
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
     const bool valid = row[q] >= 0;
     const unsigned active = __ballot_sync(0xffffffffu, valid);
     const unsigned kb = __ballot_sync(0xffffffffu, cand[q]);
     if (lane == 0 && active) keep_bits[(e0 + int64_t(warp) * 32 * PER + q * 32) >> 5] = kb;
-    if (valid) {
-      const unsigned peers = __match_any_sync(active, (unsigned long long)row[q]);
-      const int c = __popc(kb & peers);
-      if (lane == __ffs(peers) - 1 && c) atomicAdd(&deg[row[q]], c);
+    const int32_t r32 = int32_t(row[q]);
+    const int32_t prev = __shfl_up_sync(0xffffffffu, r32, 1);
+    const bool head = valid && (lane == 0 || prev != r32);
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    if (head) {
+      const unsigned after = heads & ~((2u << lane) - 1u);  // later heads
+      const unsigned run = (after ? (after & (0u - after)) - 1u : 0xffffffffu) & ~((1u << lane) - 1u);
+      const int c = __popc(kb & run);
+      if (c) atomicAdd(&deg[row[q]], c);
     }
   }
 }
@@ -651,7 +658,7 @@ __device__ __forceinline__ int tc_log_slots(int64_t d, int cap_log) {
 //    positions resolved per step, so lanes stay busy and reads coalesced.
 constexpr int TC_WIN = 4;
 constexpr int TC_LONG = 16;
-constexpr int TC_UNROLL = 4;
+constexpr int TC_UNROLL = 8;
 
 template <typename Probe>
 __device__ __forceinline__ uint32_t tc_wedges32(const int32_t* __restrict__ adj, int2 suffix,
