@@ -238,7 +238,6 @@ __global__ void __launch_bounds__(PR_THREADS) pr_spmv_kernel(
     int last_iter) {
   __shared__ double vals[PR_TILE];
   __shared__ PrRows sr;
-  __shared__ double s_red[8];
   const int64_t c = blockIdx.x;
   const int64_t e0 = c * PR_TILE;
   const int64_t e1 = min(e, e0 + PR_TILE);
@@ -284,8 +283,10 @@ __global__ void __launch_bounds__(PR_THREADS) pr_spmv_kernel(
   double dang = 0.0;
   pr_rows(vals, sr, in_off, e0, ne, first_row, nseg, has_head, has_tail, c, base, damping,
           inv_out, pos, score, contrib_next, head, tail, tail_row, last, dang);
-  dang = block_sum_256(dang, s_red);
-  if (threadIdx.x == 0) dpart[c] = dang;
+  // per-warp dangling partials (summed in a fixed order by the fixup kernel):
+  // no block-wide barrier at the end of the tile
+  dang = warp_sum(dang);
+  if ((threadIdx.x & 31) == 0) dpart[c * (PR_THREADS / 32) + (threadIdx.x >> 5)] = dang;
 }
 
 __global__ void __launch_bounds__(256) pr_fixup_kernel(
@@ -303,7 +304,8 @@ __global__ void __launch_bounds__(256) pr_fixup_kernel(
       (1.0 - damping) / double(n_total) + damping * (*dangling_prev / double(n_total));
   double dang = 0.0;
   if (c < tiles) {
-    dang = dpart[c];
+#pragma unroll
+    for (int w = 0; w < PR_THREADS / 32; ++w) dang += dpart[c * (PR_THREADS / 32) + w];
     const int64_t v = tail_row[c];
     if (v >= 0) {
       const int64_t c_last = (in_off[v + 1] - 1) / PR_TILE;
@@ -366,7 +368,7 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
   const int init_blocks = static_cast<int>(std::min<int64_t>(ceil_div64(n, 256), 4LL * ctx().sm_count));
 
   // Scratch (one allocation, carved).
-  const size_t bytes = size_t(n) * 8 * 3 + size_t(tiles + 1) * 8 * 5 + size_t(iterations + 2) * 8 +
+  const size_t bytes = size_t(n) * 8 * 3 + size_t(tiles + 1) * 8 * 12 + size_t(iterations + 2) * 8 +
                        size_t(std::max(fix_blocks, init_blocks)) * 8 + 256;
   char* p = static_cast<char*>(ws_get(WS_TMP1, bytes));
   auto carve = [&](size_t b) { char* r = p; p += (b + 15) & ~size_t(15); return r; };
@@ -377,7 +379,7 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
   double* head = reinterpret_cast<double*>(carve(size_t(tiles) * 8));
   double* tail = reinterpret_cast<double*>(carve(size_t(tiles) * 8));
   int64_t* tail_row = reinterpret_cast<int64_t*>(carve(size_t(tiles) * 8));
-  double* dpart = reinterpret_cast<double*>(carve(size_t(tiles) * 8));
+  double* dpart = reinterpret_cast<double*>(carve(size_t(tiles) * 8 * (gtd::PR_THREADS / 32)));
   double* dang = reinterpret_cast<double*>(carve(size_t(iterations + 2) * 8));
   double* partials = reinterpret_cast<double*>(carve(size_t(std::max(fix_blocks, init_blocks)) * 8));
   unsigned int* ticket = reinterpret_cast<unsigned int*>(carve(16));
@@ -474,14 +476,14 @@ static void pr_step_impl(const int64_t* in_off, const int32_t* in_adj, int64_t r
                          int last, double* score_rows, double* contrib_rows, double* dangling_out) {
   const int64_t tiles = std::max<int64_t>(1, ceil_div64(e, gtd::PR_TILE));
   const int fix_blocks = ceil_div(tiles, 256);
-  const size_t bytes = size_t(tiles + 1) * 8 * 5 + size_t(fix_blocks) * 8 + 256;
+  const size_t bytes = size_t(tiles + 1) * 8 * 12 + size_t(fix_blocks) * 8 + 256;
   char* p = static_cast<char*>(ws_get(WS_TMP1, bytes));
   auto carve = [&](size_t b) { char* r = p; p += (b + 15) & ~size_t(15); return r; };
   int64_t* tile_row = reinterpret_cast<int64_t*>(carve(size_t(tiles + 1) * 8));
   double* head = reinterpret_cast<double*>(carve(size_t(tiles) * 8));
   double* tail = reinterpret_cast<double*>(carve(size_t(tiles) * 8));
   int64_t* tail_row = reinterpret_cast<int64_t*>(carve(size_t(tiles) * 8));
-  double* dpart = reinterpret_cast<double*>(carve(size_t(tiles) * 8));
+  double* dpart = reinterpret_cast<double*>(carve(size_t(tiles) * 8 * (gtd::PR_THREADS / 32)));
   double* partials = reinterpret_cast<double*>(carve(size_t(fix_blocks) * 8));
   unsigned int* ticket = reinterpret_cast<unsigned int*>(carve(16));
   GT_CUDA(cudaMemsetAsync(ticket, 0, 16, ctx().stream));

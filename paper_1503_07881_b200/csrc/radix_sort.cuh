@@ -90,6 +90,20 @@ __device__ __forceinline__ T block_excl_scan_256(T v, T* sm, T& total) {
   return wpre + inc - v;
 }
 
+// Deterministic block sum (fixed tree) across NW warps; `sm` needs NW slots.
+template <int NW, typename T>
+__device__ __forceinline__ T block_sum_warps(T v, T* sm) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  v = warp_sum(v);
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  T tot = 0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) tot += sm[i];
+  __syncthreads();
+  return tot;
+}
+
 // Deterministic block sum (fixed tree) across 256 threads.
 template <typename T>
 __device__ __forceinline__ T block_sum_256(T v, T* sm) {
