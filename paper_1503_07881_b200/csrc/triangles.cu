@@ -50,6 +50,9 @@ constexpr int TC_WARP_MAX = TC_SLOTS / 4;      // largest d+(v) of a warp hash t
 constexpr int TC_CHUNK = 256;                  // arcs per warp task
 constexpr int TC_CHUNK_CTA = 1024;             // arcs per CTA task
 constexpr int TC_BM_BITS = TC_SLOTS * 32;      // per-warp bitmap window (same 8 KB region)
+constexpr int TC_SPLIT_TOP = TC_BM_BITS / 2;   // split tables: bitmap of the top 2^15 ranks ...
+constexpr int TC_SPLIT_SLOTS = TC_SLOTS / 2;   // ... + hash of the rest (4 KB each)
+constexpr int TC_SPLIT_MAX = TC_SPLIT_SLOTS / 4;  // largest d+(v) of a split task
 constexpr int32_t TC_EMPTY = -1;
 
 __global__ void __launch_bounds__(256) cat_off_kernel(const int64_t* __restrict__ out_off,
@@ -552,14 +555,16 @@ __global__ void __launch_bounds__(256) place_rows_kernel(
 }
 
 // ---- work lists --------------------------------------------------------------
-// kind 0: warp bitmap tasks (n-1-v <= TC_BM_BITS), 1: warp hash tasks,
-// 2: CTA hash tasks. A task is (v, chunk of N-(v)); it needs d+(v), d-(v) >= 1.
+// kind 0: warp bitmap tasks (n-1-v <= TC_BM_BITS), 3: warp split tasks
+// (d+(v) <= TC_SPLIT_MAX), 1: warp hash tasks, 2: CTA hash tasks. A task is (v, chunk of N-(v)); it needs d+(v), d-(v) >= 1.
 __global__ void __launch_bounds__(256) tc_task_count_kernel(const int64_t* __restrict__ off_p,
                                                             const int64_t* __restrict__ off_m,
                                                             int64_t n, int part, int nparts,
+                                                            int64_t bm_bits,
                                                             int64_t* __restrict__ c0,
                                                             int64_t* __restrict__ c1,
-                                                            int64_t* __restrict__ c2) {
+                                                            int64_t* __restrict__ c2,
+                                                            int64_t* __restrict__ c3) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n) return;
   const int64_t dp = off_p[v + 1] - off_p[v];
@@ -567,9 +572,11 @@ __global__ void __launch_bounds__(256) tc_task_count_kernel(const int64_t* __res
   // a part owns whole N-(v) lists (v = part mod nparts): the order inside a
   // list is scheduling dependent, so chunks of one list must stay together
   const bool live = dp >= 1 && dm >= 1 && v % nparts == part;
-  const bool bm = n - 1 - v <= TC_BM_BITS;
+  const bool bm = n - 1 - v <= bm_bits;
   c0[v] = (live && bm) ? (dm + TC_CHUNK - 1) / TC_CHUNK : 0;
-  c1[v] = (live && !bm && dp <= TC_WARP_MAX) ? (dm + TC_CHUNK - 1) / TC_CHUNK : 0;
+  c1[v] = (live && !bm && dp > TC_SPLIT_MAX && dp <= TC_WARP_MAX)
+              ? (dm + TC_CHUNK - 1) / TC_CHUNK : 0;
+  c3[v] = (live && !bm && dp <= TC_SPLIT_MAX) ? (dm + TC_CHUNK - 1) / TC_CHUNK : 0;
   c2[v] = (live && !bm && dp > TC_WARP_MAX) ? (dm + TC_CHUNK_CTA - 1) / TC_CHUNK_CTA : 0;
 }
 
@@ -639,6 +646,31 @@ struct BitmapProbe {
     uint32_t x;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(sbase + ((i >> 5) << 2)) : "memory");
     return (x >> (i & 31)) & 1u;
+  }
+};
+
+// Split table for v below the bitmap window: the members of N+(v) among the
+// top TC_SPLIT_TOP ranks in a bitmap (where R-MAT sends nearly every probe),
+// the others in a small open-addressing hash (load <= 1/4).
+struct SplitProbe {
+  uint32_t sbm;   // shared address of the bitmap words
+  uint32_t stab;  // shared address of the hash slots
+  int32_t top;    // n - TC_SPLIT_TOP
+  __device__ __forceinline__ bool operator()(int32_t w) const {
+    uint32_t x;
+    if (w >= top) {
+      const uint32_t i = uint32_t(w - top);
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(sbm + ((i >> 5) << 2)) : "memory");
+      return (x >> (i & 31)) & 1u;
+    }
+    constexpr int L = 10;  // log2(TC_SPLIT_SLOTS)
+    uint32_t h = tc_hash(w, L);
+    while (true) {
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(stab + (h << 2)) : "memory");
+      if (int32_t(x) == w) return true;
+      if (int32_t(x) == TC_EMPTY) return false;
+      h = (h + 1) & (TC_SPLIT_SLOTS - 1);
+    }
   }
 };
 
@@ -758,8 +790,8 @@ __device__ __forceinline__ uint32_t tc_wedges32(const int32_t* __restrict__ adj,
 __global__ void __launch_bounds__(256) tc_count_warp_kernel(
     const int64_t* __restrict__ off_p, const int32_t* __restrict__ adj_p,
     const int64_t* __restrict__ off_m, const int2* __restrict__ nm,
-    const int2* __restrict__ tasks, int64_t n_bitmap_tasks, int64_t n_tasks, int64_t n,
-    int part, int nparts, unsigned int* __restrict__ next_task,
+    const int2* __restrict__ tasks, int64_t n_bitmap_tasks, int64_t n_split_end, int64_t n_tasks,
+    int64_t n, int split_top, int part, int nparts, unsigned int* __restrict__ next_task,
     unsigned long long* __restrict__ total) {
   extern __shared__ int32_t s_tab[];  // [8][TC_SLOTS]
   __shared__ uint8_t s_start[8][32 * TC_WIN];
@@ -778,10 +810,24 @@ __global__ void __launch_bounds__(256) tc_count_warp_kernel(
     const int2 task = tasks[it];
     const int v = task.x;
     const bool use_bm = it < n_bitmap_tasks;
+    const bool use_split = !use_bm && it < n_split_end;
     if (v != cur_v) {
       const int64_t ov = off_p[v];
       const int dv = int(off_p[v + 1] - ov);
-      if (use_bm) {
+      if (use_split) {
+        const int32_t top = int32_t(n - split_top);
+        uint32_t* sbm = reinterpret_cast<uint32_t*>(tab);
+        int32_t* stab = tab + TC_SPLIT_TOP / 32;
+        for (int i = lane; i < TC_SPLIT_TOP / 32; i += 32) sbm[i] = 0u;
+        for (int i = lane; i < TC_SPLIT_SLOTS; i += 32) stab[i] = TC_EMPTY;
+        __syncwarp();
+        const HashProbe low{stab, TC_SPLIT_SLOTS - 1u, 10};
+        for (int i = lane; i < dv; i += 32) {
+          const int32_t x = adj_p[ov + i];
+          if (x >= top) atomicOr(&sbm[uint32_t(x - top) >> 5], 1u << (uint32_t(x - top) & 31));
+          else low.insert(x);
+        }
+      } else if (use_bm) {
         const int nwords = int((n - 1 - v + 31) >> 5);
         for (int i = lane; i < nwords; i += 32) bm[i] = 0u;
         __syncwarp();
@@ -803,7 +849,15 @@ __global__ void __launch_bounds__(256) tc_count_warp_kernel(
     const int dm = int(off_m[v + 1] - om);
     const int end = min(dm, (task.y + 1) * TC_CHUNK);
     uint32_t cnt = 0;
-    if (use_bm) {
+    if (use_split) {
+      const uint32_t sb = uint32_t(__cvta_generic_to_shared(tab));
+      const SplitProbe probe{sb, sb + TC_SPLIT_TOP / 8, int32_t(n - split_top)};
+      for (int jb = task.y * TC_CHUNK; jb < end; jb += 32) {
+        const int jj = jb + lane;
+        const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
+        cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
+      }
+    } else if (use_bm) {
       const BitmapProbe probe{uint32_t(__cvta_generic_to_shared(bm)), v + 1};
       for (int jb = task.y * TC_CHUNK; jb < end; jb += 32) {
         const int jj = jb + lane;
@@ -823,39 +877,73 @@ __global__ void __launch_bounds__(256) tc_count_warp_kernel(
   if (lane == 0 && acc) atomicAdd(total, acc);
 }
 
-// Hash tasks with large d+(v), CTA per (v, chunk); table in dynamic shared
-// memory, or in `gtab` (2^log_slots per CTA) when it does not fit.
+// Tasks with large d+(v) below the bitmap window, CTA per (v, chunk). N+(v)
+// goes to a hash table as sparse as shared memory allows (TC_CTA_SLOTS slots,
+// probed with shared-window loads: nearly every miss resolves in one probe),
+// or, when 2 d+(v) exceeds that, to a per-CTA global table of gtab_slots.
+constexpr int TC_CTA_SLOTS = 1 << 14;  // 64 KB: 3 CTAs per SM
+
+struct SmemHashProbe {
+  uint32_t stab;  // shared address of the slots
+  uint32_t mask;
+  int log_slots;
+  __device__ __forceinline__ bool operator()(int32_t w) const {
+    uint32_t h = tc_hash(w, log_slots);
+    while (true) {
+      uint32_t x;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(stab + (h << 2)) : "memory");
+      if (int32_t(x) == w) return true;
+      if (int32_t(x) == TC_EMPTY) return false;
+      h = (h + 1) & mask;
+    }
+  }
+};
+
 __global__ void __launch_bounds__(256) tc_count_cta_kernel(
     const int64_t* __restrict__ off_p, const int32_t* __restrict__ adj_p,
     const int64_t* __restrict__ off_m, const int2* __restrict__ nm,
-    const int2* __restrict__ tasks, int64_t n_tasks, int log_slots, int32_t* __restrict__ gtab,
-    int part, int nparts, unsigned long long* __restrict__ total) {
-  extern __shared__ int32_t s_dyn[];
+    const int2* __restrict__ tasks, int64_t n_tasks, int smem_log, int32_t* __restrict__ gtab,
+    int gtab_log, unsigned long long* __restrict__ total) {
+  extern __shared__ __align__(16) int32_t s_cta[];
   __shared__ uint8_t s_start[8][32 * TC_WIN];
   __shared__ unsigned long long s_red[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int32_t* tab = gtab ? gtab + (int64_t(blockIdx.x) << log_slots) : s_dyn;
-  const HashProbe probe{tab, (1u << log_slots) - 1u, log_slots};
+  int32_t* mytab = gtab ? gtab + (int64_t(blockIdx.x) << gtab_log) : nullptr;
   unsigned long long acc = 0;
   for (int64_t it = blockIdx.x; it < n_tasks; it += gridDim.x) {
     const int2 task = tasks[it];
     const int v = task.x;
     const int64_t ov = off_p[v];
     const int dv = int(off_p[v + 1] - ov);
+    const bool in_smem = 2 * int64_t(dv) <= (int64_t(1) << smem_log);
+    const int log_slots = in_smem ? smem_log : gtab_log;
+    int32_t* tab = in_smem ? s_cta : mytab;
+    const int slots = 1 << log_slots;
     __syncthreads();  // previous task done with the table
-    for (int i = threadIdx.x; i <= int(probe.mask); i += 256) tab[i] = TC_EMPTY;
+    for (int i = threadIdx.x; i < slots; i += 256) tab[i] = TC_EMPTY;
     __syncthreads();
-    for (int i = threadIdx.x; i < dv; i += 256) probe.insert(adj_p[ov + i]);
+    const HashProbe ins{tab, uint32_t(slots - 1), log_slots};
+    for (int i = threadIdx.x; i < dv; i += 256) ins.insert(adj_p[ov + i]);
     __syncthreads();
     const int64_t om = off_m[v];
     const int dm = int(off_m[v + 1] - om);
     const int begin = task.y * TC_CHUNK_CTA;
     const int end = min(dm, begin + TC_CHUNK_CTA);
     uint32_t cnt = 0;
-    for (int jb = begin + warp * 32; jb < end; jb += 256) {
-      const int jj = jb + lane;
-      const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
-      cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
+    if (in_smem) {
+      const SmemHashProbe probe{uint32_t(__cvta_generic_to_shared(tab)), uint32_t(slots - 1),
+                                log_slots};
+      for (int jb = begin + warp * 32; jb < end; jb += 256) {
+        const int jj = jb + lane;
+        const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
+        cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
+      }
+    } else {
+      for (int jb = begin + warp * 32; jb < end; jb += 256) {
+        const int jj = jb + lane;
+        const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
+        cnt += tc_wedges32(adj_p, sfx, ins, s_start[warp]);
+      }
     }
     acc += cnt;
   }
@@ -1101,33 +1189,44 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
   int64_t* off_m = o.off_m;
   const int2* nm = o.nm;
   // work-list scratch
-  char* p = static_cast<char*>(ws_get(WS_COLS, size_t(n + 1) * 8 * 3 + 64));
+  char* p = static_cast<char*>(ws_get(WS_COLS, size_t(n + 1) * 8 * 4 + 96));
   auto carve = [&](size_t b) { char* r = p; p += (b + 15) & ~size_t(15); return r; };
   int64_t* t0 = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
   int64_t* t1 = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
   int64_t* t2 = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
+  int64_t* t3 = reinterpret_cast<int64_t*>(carve(size_t(n + 1) * 8));
+  // table windows; GT_TC_WINDOW (ranks, power of two >= 64) shrinks them so
+  // that small test graphs exercise the split / hash / CTA paths
+  int64_t bm_bits = gtd::TC_BM_BITS;
+  if (const char* env = getenv("GT_TC_WINDOW")) bm_bits = std::max<int64_t>(64, atoll(env));
+  bm_bits = std::min<int64_t>(bm_bits, gtd::TC_BM_BITS);
+  const int split_top = int(std::min<int64_t>(bm_bits / 2, gtd::TC_SPLIT_TOP));
   // 6. work lists
   {
     Phase ph("tc.tasks", 8.0 * (n + 1) * 8);
     GT_CUDA(cudaMemsetAsync(small + 14, 0, 16, s));
     GT_LAUNCH(gtd::tc_task_count_kernel, ceil_div(n, 256), 256, 0, o.off_p, off_m, n, part, nparts,
-              t0, t1, t2);
+              bm_bits, t0, t1, t2, t3);
     exclusive_scan_i64(t0, n, small + 8);
     exclusive_scan_i64(t1, n, small + 9);
     exclusive_scan_i64(t2, n, small + 10);
+    exclusive_scan_i64(t3, n, small + 11);
     GT_LAUNCH(gtd::max_dplus_kernel, grid_cap(ceil_div64(n, 256)), 256, 0, o.off_p, n,
               reinterpret_cast<unsigned long long*>(small + 14));  // [14] max d+, [15] probes
   }
   int64_t h[8];
   d2h(h, small + 8, sizeof h);  // bitmap / warp / CTA task counts, ..., max d+, probes
   sync();
-  const int64_t n_bm = h[0], n_wt = h[1], n_ct = h[2], max_dp = h[6], probes = h[7];
+  const int64_t n_bm = h[0], n_hw = h[1], n_ct = h[2], n_sp = h[3], max_dp = h[6], probes = h[7];
+  const int64_t n_wt = n_sp + n_hw;  // warp tasks after the bitmap ones: split, then hash
   if (n_bm + n_wt + n_ct >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangle work list too long");
   int2* tasks = ws_n<int2>(WS_TMP2, size_t(n_bm + n_wt + n_ct) + 1);  // buf is dead by now
   {
     Phase ph("tc.tasks", 8.0 * (n_bm + n_wt + n_ct));
     if (n_bm) GT_LAUNCH(gtd::tc_task_fill_kernel, ceil_div(n, 256), 256, 0, t0, n, tasks);
-    if (n_wt) GT_LAUNCH(gtd::tc_task_fill_kernel, ceil_div(n, 256), 256, 0, t1, n, tasks + n_bm);
+    if (n_sp) GT_LAUNCH(gtd::tc_task_fill_kernel, ceil_div(n, 256), 256, 0, t3, n, tasks + n_bm);
+    if (n_hw)
+      GT_LAUNCH(gtd::tc_task_fill_kernel, ceil_div(n, 256), 256, 0, t1, n, tasks + n_bm + n_sp);
     if (n_ct)
       GT_LAUNCH(gtd::tc_task_fill_kernel, ceil_div(n, 256), 256, 0, t2, n, tasks + n_bm + n_wt);
   }
@@ -1142,30 +1241,30 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
     GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_warp_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     GT_LAUNCH(gtd::tc_count_warp_kernel, ctx().sm_count * 3, 256, smem, o.off_p, o.adj_p, off_m,
-              nm, tasks, n_bm, n_bm + n_wt, n, part, nparts, counters + 22, total);
+              nm, tasks, n_bm, n_bm + n_sp, n_bm + n_wt, n, split_top, part, nparts, counters + 22,
+              total);
   }
   if (n_ct) {
     Phase ph("tc.count_hash", 0.0);
-    int log_slots = 5;
-    while ((int64_t(1) << log_slots) < 4 * max_dp) ++log_slots;
-    const size_t tab_bytes = size_t(4) << log_slots;
-    const int grid = static_cast<int>(std::min<int64_t>(n_ct, 2LL * ctx().sm_count));
-    // GT_TC_TABLE_SMEM_MAX (bytes) lowers the shared-memory cap (tests drive
-    // the global-table path with it).
-    size_t smem_cap = 160 * 1024;
-    if (const char* env = getenv("GT_TC_TABLE_SMEM_MAX")) smem_cap = size_t(atoll(env));
+    // GT_TC_TABLE_SMEM_MAX (bytes) shrinks the shared table (tests drive the
+    // global-table path with it)
+    size_t cap = size_t(gtd::TC_CTA_SLOTS) * 4;
+    if (const char* env = getenv("GT_TC_TABLE_SMEM_MAX")) cap = std::min(cap, size_t(atoll(env)));
+    int smem_log = 5;
+    while ((size_t(4) << (smem_log + 1)) <= cap) ++smem_log;
+    const int smem = 4 << smem_log;
+    GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_cta_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int grid = static_cast<int>(std::min<int64_t>(n_ct, 3LL * ctx().sm_count));
     int32_t* gtab = nullptr;
-    size_t smem = 0;
-    if (tab_bytes <= smem_cap) {
-      smem = tab_bytes;
-      if (smem > 48 * 1024)
-        GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_cta_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    } else {
-      gtab = ws_n<int32_t>(WS_TMP4, size_t(grid) << log_slots);
+    int gtab_log = 0;
+    if (2 * max_dp > (int64_t(1) << smem_log)) {
+      gtab_log = 5;
+      while ((int64_t(1) << gtab_log) < 8 * max_dp) ++gtab_log;
+      gtab = ws_n<int32_t>(WS_TMP4, size_t(grid) << gtab_log);
     }
     GT_LAUNCH(gtd::tc_count_cta_kernel, grid, 256, smem, o.off_p, o.adj_p, off_m, nm,
-              tasks + n_bm + n_wt, n_ct, log_slots, gtab, part, nparts, total);
+              tasks + n_bm + n_wt, n_ct, smem_log, gtab, gtab_log, total);
   }
   int64_t result = 0;
   d2h(&result, total, 8);

@@ -95,11 +95,14 @@ def test_c3_full_vs_oracle():
     assert gt.triangle_count(g) == want
 
 
-@pytest.mark.parametrize("smem_cap", [None, "1024"])
-def test_hub_orientation_cta_path(monkeypatch, smem_cap):
-    """K_n with n > 2*TC_WARP_MAX: oriented out-degrees above the per-warp
-    table size go through the CTA kernel (shared-memory table, or the global
-    scratch table when GT_TC_TABLE_SMEM_MAX forces it)."""
+@pytest.mark.parametrize("window,smem_cap", [(None, None), ("64", None), ("64", "1024"),
+                                             ("256", None)])
+def test_hub_orientation_all_table_paths(monkeypatch, window, smem_cap):
+    """K_n with n = 1200: oriented out-degrees 0..1199. GT_TC_WINDOW shrinks
+    the bitmap window so that the split (bitmap + hash), warp-hash and CTA
+    paths all run; GT_TC_TABLE_SMEM_MAX forces the CTA path's global table."""
+    if window is not None:
+        monkeypatch.setenv("GT_TC_WINDOW", window)
     if smem_cap is not None:
         monkeypatch.setenv("GT_TC_TABLE_SMEM_MAX", smem_cap)
     n = 1200
@@ -109,6 +112,16 @@ def test_hub_orientation_cta_path(monkeypatch, smem_cap):
     src = np.where(flip, b, a) * 7 + 3
     dst = np.where(flip, a, b) * 7 + 3
     want = n * (n - 1) * (n - 2) // 6
+    assert gt.triangle_count(build(src, dst)) == want
+
+
+@pytest.mark.parametrize("window", ["64", "1024"])
+def test_small_windows_match_reference_on_rmat(monkeypatch, window):
+    from paper_1503_07881_b200.synth import rmat_edges
+
+    monkeypatch.setenv("GT_TC_WINDOW", window)
+    src, dst = rmat_edges(13, 60000, seed=12, permute=True)
+    want = ref.triangle_count_fast(ref.build_csr(src, dst))
     assert gt.triangle_count(build(src, dst)) == want
 
 
