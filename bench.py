@@ -338,6 +338,25 @@ def ours_arm(args):
                 "ms_per_launch": dom_ms / max(dom_cnt, 1), "peak_source": pk["source"],
                 "share_of_step": dom_ms / elapsed_ms}
 
+    # ---- §8f next #1: graph -> edge table export (device), measured apart ----
+    extras = {}
+    if not sharded:
+        g_x = gt.table_to_graph(table, edge_spec)
+        _native.profile_reset()
+        _native.profile_enable(True)
+        for _ in range(args.steps):
+            gt.graph_to_edge_table(g_x, device=True)
+        ph_x = _native.profile_read()
+        _native.profile_enable(False)
+        ms_x, _, by_x = ph_x.get("export.edges", (0.0, 0, 0.0))
+        if ms_x > 0:
+            ms_x /= args.steps
+            extras["graph_to_edge_table"] = {
+                "ms": ms_x, "value": g_x.edge_count / (ms_x / 1e3), "unit": "edges/s",
+                "achieved_gbs": by_x / args.steps / (ms_x / 1e3) / 1e9,
+                "hbm_frac": by_x / args.steps / (ms_x / 1e3) / 1e9 / pk["hbm_gbs"]}
+        del g_x
+
     # ---- end to end through the public API with host buffers ---------------
     e2e = None
     if not args.no_e2e:
@@ -416,7 +435,7 @@ def ours_arm(args):
                    "parallelism": f"sharded x{world} (NCCL)" if sharded else "single",
                    "rows_per_gpu": rows,
                    "l2": "inputs larger than L2 (16*rows bytes >> 126 MB)"},
-        "phases": phase_line, "kernels": kernels, "roofline": roofline,
+        "phases": phase_line, "extras": extras, "kernels": kernels, "roofline": roofline,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks.summary(),
     }

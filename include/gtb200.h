@@ -106,6 +106,18 @@ GT_API int gt_graph_device_views(const gt_graph* g, const int64_t** d_ids,
 
 GT_API void gt_graph_free(gt_graph* g);
 
+/* ---- graph -> table (convert.py:178-217) ----------- */
+
+/* The edge table of the graph, sorted by (src, dst), original ids
+ * (graph_to_edge_table, convert.py:178-197): src[E], dst[E], host or device
+ * buffers. */
+GT_API int gt_graph_edge_table(const gt_graph* g, int64_t* src, int64_t* dst, int out_is_device);
+
+/* The node table (node, out_deg, in_deg), ascending by id
+ * (graph_to_node_table, convert.py:200-217): three int64[N] buffers. */
+GT_API int gt_graph_node_table(const gt_graph* g, int64_t* node, int64_t* out_deg,
+                               int64_t* in_deg, int out_is_device);
+
 /* ---- PageRank (algorithms.pagerank, algorithms.py:36-87) --------------- */
 
 /* Damped power iteration, fp64, start 1/N, dangling mass redistributed

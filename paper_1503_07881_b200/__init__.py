@@ -10,7 +10,7 @@ the GPU, calling the path without the library raises ``NativeError``.
 """
 
 from .algorithms import RankMap, pagerank, pagerank_device, triangle_count
-from .convert import EdgeSpec, table_to_graph
+from .convert import EdgeSpec, graph_to_edge_table, graph_to_node_table, table_to_graph
 from .errors import (
     CapacityError,
     CoverageError,
@@ -23,7 +23,8 @@ from .errors import (
     UnknownNodeError,
 )
 from .graph import DeviceGraph, Graph, NodeRecord, from_edges, upload
-from .tables import FLOAT, INT, STRING, ColumnTable, Schema, edge_table, load_tsv, save_tsv
+from .tables import (FLOAT, INT, STRING, ColumnTable, Schema, edge_table, load_tsv, save_tsv,
+                     table_from_map)
 
 __version__ = "0.1.0"
 
@@ -31,6 +32,7 @@ __all__ = [
     "CapacityError", "ColumnTable", "CoverageError", "DeviceGraph", "EdgeSpec", "EngineError",
     "FLOAT", "Graph", "INT", "NativeError", "NodeRecord", "ParseError", "RankMap", "STRING",
     "Schema", "SchemaError", "TypeMismatchError", "UnknownColumnError", "UnknownNodeError",
-    "edge_table", "from_edges", "load_tsv", "pagerank", "pagerank_device", "save_tsv",
-    "table_to_graph", "triangle_count", "upload",
+    "edge_table", "from_edges", "graph_to_edge_table", "graph_to_node_table", "load_tsv",
+    "pagerank", "pagerank_device", "save_tsv", "table_from_map", "table_to_graph",
+    "triangle_count", "upload",
 ]

@@ -39,6 +39,8 @@ SIGNATURES = {
                                              ctypes.POINTER(_VP)]),
     "gt_graph_free": (None, [_VP]),
     "gt_pagerank": (ctypes.c_int, [_VP, ctypes.c_double, ctypes.c_int, _VP, ctypes.c_int]),
+    "gt_graph_edge_table": (ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int]),
+    "gt_graph_node_table": (ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int]),
     "gt_triangles": (ctypes.c_int, [_VP, _I64P]),
     "gt_triangle_orientation": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _I64P]),
     "gt_rmat_generate": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_double,
@@ -226,6 +228,20 @@ def triangle_orientation(handle: int, n: int):
     check(lib.gt_triangle_orientation(handle, None, None, None, _ptr(adj_p), ctypes.byref(m)),
           "gt_triangle_orientation")
     return deg, rank, off_p, adj_p
+
+
+def graph_edge_table(handle: int, src, dst, on_device: bool):
+    lib = ensure_init()
+    if on_device:
+        check(lib.gt_graph_edge_table(handle, int(src), int(dst), 1), "gt_graph_edge_table")
+    else:
+        check(lib.gt_graph_edge_table(handle, _ptr(src), _ptr(dst), 0), "gt_graph_edge_table")
+
+
+def graph_node_table(handle: int, node, out_deg, in_deg):
+    lib = ensure_init()
+    check(lib.gt_graph_node_table(handle, _ptr(node), _ptr(out_deg), _ptr(in_deg), 0),
+          "gt_graph_node_table")
 
 
 def rmat_generate(scale, rows, a, b, c, seed, permute, src_ptr, dst_ptr, start=0):

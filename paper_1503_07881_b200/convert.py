@@ -83,3 +83,75 @@ def table_to_graph(table, spec: EdgeSpec, workers: int | None = None) -> DeviceG
             dst = dst.cpu().numpy()
         handle = _native.build_csr(np.asarray(src), np.asarray(dst), rows, False)
     return DeviceGraph(handle)
+
+
+# ------------------------------------------------------------ graph -> table
+# the step after the path in the paper's workflow
+# (demo.py:45-46). Device kernels in libgtb200 (gt_graph_edge_table /
+# gt_graph_node_table); host graphs are uploaded first.
+
+def graph_to_edge_table(g, workers: int | None = None, device: bool = False):
+    """Edges as a two-column table sorted by (src, dst) (convert.py:178-197).
+
+    ``device=True`` leaves the columns in HBM (torch tensors)."""
+    from .graph import upload
+    from .tables import ColumnTable, Schema
+
+    resolve_workers(workers)
+    dg = upload(g)
+    e = dg.edge_count
+    schema = Schema([("src", INT), ("dst", INT)])
+    if device:
+        import torch
+
+        src = torch.empty(e, dtype=torch.int64, device="cuda")
+        dst = torch.empty(e, dtype=torch.int64, device="cuda")
+        _native.graph_edge_table(dg.handle, src.data_ptr(), dst.data_ptr(), True)
+    else:
+        src = np.empty(e, dtype=np.int64)
+        dst = np.empty(e, dtype=np.int64)
+        _native.graph_edge_table(dg.handle, src, dst, False)
+    return ColumnTable(schema, [src, dst])
+
+
+def graph_to_node_table(g, values=None, value_name: str = "value"):
+    """Per-node table (node, out_deg, in_deg[, value]), ascending by id
+    (convert.py:200-217); ``values`` must cover exactly the node set
+    (CoverageError otherwise)."""
+    from .errors import CoverageError
+    from .graph import upload
+    from .tables import FLOAT, ColumnTable, Schema
+
+    dg = upload(g)
+    n = dg.node_count
+    node = np.empty(n, dtype=np.int64)
+    out_deg = np.empty(n, dtype=np.int64)
+    in_deg = np.empty(n, dtype=np.int64)
+    _native.graph_node_table(dg.handle, node, out_deg, in_deg)
+    cols = [node, out_deg, in_deg]
+    schema_cols = [("node", INT), ("out_deg", INT), ("in_deg", INT)]
+    if values is not None:
+        vals = _values_in_id_order(values, node)
+        if vals is None:
+            raise CoverageError(
+                "values mapping must cover exactly the node set "
+                f"({len(values)} values for {n} nodes)")
+        cols.append(vals)
+        schema_cols.append((value_name, FLOAT))
+    return ColumnTable(Schema(schema_cols), cols)
+
+
+def _values_in_id_order(values, node):
+    """float64 values aligned with `node` (ascending ids), or None when the
+    key set differs from the node set."""
+    ids = getattr(values, "ids", None)
+    if ids is not None and hasattr(values, "scores"):  # RankMap: already (ids, scores)
+        if np.array_equal(np.asarray(ids), node):
+            return np.asarray(values.scores, dtype=np.float64)
+        return None
+    if len(values) != node.shape[0]:
+        return None
+    try:
+        return np.asarray([float(values[int(i)]) for i in node.tolist()], dtype=np.float64)
+    except KeyError:
+        return None

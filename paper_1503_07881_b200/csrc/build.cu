@@ -827,3 +827,140 @@ int gt_graph_from_csr(int64_t n, int64_t e, const int64_t* d_ids, const int64_t*
 }
 
 }  // extern "C"
+
+// ============================================================================
+// Graph -> table (convert.py:178-217): the out-CSR
+// expanded back into an edge table sorted by (src, dst), and the per-node
+// table (node, out_deg, in_deg). Pure bandwidth: per edge 4 B adjacency +
+// two id gathers in, 16 B out.
+// ============================================================================
+namespace gtd {
+
+// Edge tiles of 2048 (coalesced: edge e0 + 256*q + tid): the tile's row
+// offsets are staged in shared memory, each edge finds its row by a short
+// binary search there, dst = ids[adj] is a gather from L2, src = ids[row]
+// hits L1 (consecutive edges share rows).
+constexpr int EXPORT_TILE = 2048;
+constexpr int EXPORT_ROWS = EXPORT_TILE + 2;
+
+__global__ void __launch_bounds__(256) export_tile_rows_kernel(const int64_t* __restrict__ off,
+                                                               int64_t n, int64_t e,
+                                                               int64_t tiles,
+                                                               int64_t* __restrict__ tile_row) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t > tiles) return;
+  const int64_t x = t < tiles ? t * EXPORT_TILE : e - 1;  // row holding edge x
+  int64_t lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  tile_row[t] = lo;
+}
+
+__global__ void __launch_bounds__(256) edge_table_kernel(const int64_t* __restrict__ ids,
+                                                         const int64_t* __restrict__ off,
+                                                         const int32_t* __restrict__ adj,
+                                                         int64_t e,
+                                                         const int64_t* __restrict__ tile_row,
+                                                         int64_t* __restrict__ src,
+                                                         int64_t* __restrict__ dst) {
+  __shared__ int64_t s_off[EXPORT_ROWS];
+  const int64_t t = blockIdx.x;
+  const int64_t e0 = t * EXPORT_TILE;
+  const int64_t r0 = tile_row[t], r1 = tile_row[t + 1];
+  const int64_t nr = r1 - r0 + 2;
+  const bool staged = nr <= EXPORT_ROWS;
+  if (staged)
+    for (int i = threadIdx.x; i < int(nr); i += 256) s_off[i] = off[r0 + i];
+  __syncthreads();
+#pragma unroll 4
+  for (int q = 0; q < EXPORT_TILE / 256; ++q) {
+    const int64_t k = e0 + q * 256 + threadIdx.x;
+    if (k >= e) break;
+    int64_t lo = r0, hi = r1;  // largest r with off[r] <= k
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if ((staged ? s_off[mid - r0] : off[mid]) <= k) lo = mid;
+      else hi = mid - 1;
+    }
+    src[k] = ids[lo];
+    dst[k] = ids[__ldcs(adj + k)];
+  }
+}
+
+__global__ void __launch_bounds__(256) node_table_kernel(const int64_t* __restrict__ out_off,
+                                                         const int64_t* __restrict__ in_off,
+                                                         int64_t n, int64_t* __restrict__ out_deg,
+                                                         int64_t* __restrict__ in_deg) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out_deg[i] = out_off[i + 1] - out_off[i];
+  in_deg[i] = in_off[i + 1] - in_off[i];
+}
+
+}  // namespace gtd
+
+extern "C" {
+
+int gt_graph_edge_table(const gt_graph* g, int64_t* src, int64_t* dst, int out_is_device) {
+  GT_API_BEGIN
+  require_init();
+  if (!g) fail(GT_EINVAL, "null graph");
+  if (g->e == 0) return GT_OK;
+  if (!src || !dst) fail(GT_EINVAL, "output pointers must not be NULL");
+  int64_t* ds = src;
+  int64_t* dd = dst;
+  if (!out_is_device) {
+    ds = ws_n<int64_t>(WS_TMP0, size_t(2 * g->e));
+    dd = ds + g->e;
+  }
+  {
+    Phase ph("export.edges", 4.0 * g->e + 16.0 * g->e + 8.0 * g->n * 2);
+    const int64_t tiles = ceil_div64(g->e, gtd::EXPORT_TILE);
+    int64_t* tile_row = ws_n<int64_t>(WS_TMP1, size_t(tiles) + 1);
+    GT_LAUNCH(gtd::export_tile_rows_kernel, ceil_div(tiles + 1, 256), 256, 0, g->out_off, g->n,
+              g->e, tiles, tile_row);
+    GT_LAUNCH(gtd::edge_table_kernel, static_cast<int>(tiles), 256, 0, g->ids, g->out_off,
+              g->out_adj, g->e, tile_row, ds, dd);
+  }
+  if (!out_is_device) {
+    d2h(src, ds, size_t(g->e) * 8);
+    d2h(dst, dd, size_t(g->e) * 8);
+  }
+  sync();
+  GT_API_END
+}
+
+int gt_graph_node_table(const gt_graph* g, int64_t* node, int64_t* out_deg, int64_t* in_deg,
+                        int out_is_device) {
+  GT_API_BEGIN
+  require_init();
+  if (!g) fail(GT_EINVAL, "null graph");
+  if (g->n == 0) return GT_OK;
+  if (!node || !out_deg || !in_deg) fail(GT_EINVAL, "output pointers must not be NULL");
+  int64_t* od = out_deg;
+  int64_t* id = in_deg;
+  if (!out_is_device) {
+    od = ws_n<int64_t>(WS_TMP0, size_t(2 * g->n));
+    id = od + g->n;
+  }
+  {
+    Phase ph("export.nodes", 8.0 * (g->n + 1) * 2 + 16.0 * g->n);
+    GT_LAUNCH(gtd::node_table_kernel, ceil_div(g->n, 256), 256, 0, g->out_off, g->in_off, g->n,
+              od, id);
+  }
+  if (out_is_device) {
+    GT_CUDA(cudaMemcpyAsync(node, g->ids, size_t(g->n) * 8, cudaMemcpyDeviceToDevice,
+                            ctx().stream));
+  } else {
+    d2h(node, g->ids, size_t(g->n) * 8);
+    d2h(out_deg, od, size_t(g->n) * 8);
+    d2h(in_deg, id, size_t(g->n) * 8);
+  }
+  sync();
+  GT_API_END
+}
+
+}  // extern "C"

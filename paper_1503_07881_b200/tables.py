@@ -185,3 +185,20 @@ def save_tsv(table: ColumnTable, path) -> None:
 def edge_table(src, dst, names=("src", "dst")) -> ColumnTable:
     """Two-int-column edge table from arrays (host or device)."""
     return ColumnTable(Schema([(names[0], INT), (names[1], INT)]), [src, dst])
+
+
+def table_from_map(pairs, key_name: str, val_name: str) -> ColumnTable:
+    """Two-column (int key, float value) table sorted ascending by key
+    (tables.py:662-670). A PageRank ``RankMap`` is already (ids ascending,
+    scores): its arrays become the columns without a Python pass."""
+    schema = Schema([(key_name, INT), (val_name, FLOAT)])
+    ids = getattr(pairs, "ids", None)
+    if ids is not None and hasattr(pairs, "scores"):
+        return ColumnTable(schema, [np.asarray(ids, dtype=np.int64).copy(),
+                                    np.asarray(pairs.scores, dtype=np.float64).copy()])
+    items = sorted((int(k), float(v)) for k, v in pairs.items())
+    if not items:
+        return ColumnTable(schema, [np.empty(0, dtype=np.int64), np.empty(0, dtype=np.float64)])
+    keys, vals = zip(*items)
+    return ColumnTable(schema, [np.asarray(keys, dtype=np.int64),
+                                np.asarray(vals, dtype=np.float64)])
