@@ -50,6 +50,8 @@ def parse_args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-rows", type=int, default=1_000_000)
+    p.add_argument("--no-tsv", action="store_true")
+    p.add_argument("--tsv-rows", type=int, default=4_000_000)
     p.add_argument("--sharded", action="store_true",
                    help="use the multi-GPU (distributed.py) pipeline even on one GPU")
     return p.parse_args()
@@ -150,6 +152,52 @@ def reference_arm(args):
 
 
 # ----------------------------------------------------------------------- ours
+
+def tsv_extra(src, dst, args, pk):
+    """§8f next #2: LoadTableTSV of an int64 edge TSV on the GPU (file read +
+    H2D + parse, wall clock) and the parse kernels alone, on the first
+    args.tsv_rows rows of the table; the host (reference-semantics) parser on
+    a 10x smaller prefix as the CPU baseline."""
+    import torch
+
+    from paper_1503_07881_b200 import _native
+    from paper_1503_07881_b200.tables import INT, Schema, load_tsv
+
+    n = min(args.tsv_rows, int(src.shape[0]))
+    a = src[:n].cpu().numpy()
+    b = dst[:n].cpu().numpy()
+    text = ("\n".join(f"{x}\t{y}" for x, y in zip(a.tolist(), b.tolist())) + "\n").encode()
+    schema = Schema([("src", INT), ("dst", INT)])
+    with tempfile.TemporaryDirectory() as tmp:
+        path = Path(tmp) / "edges.tsv"
+        path.write_bytes(text)
+        load_tsv(path, schema, device="cuda")  # warm
+        _native.profile_reset()
+        _native.profile_enable(True)
+        reps = 3
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            t = load_tsv(path, schema, device="cuda")
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) / reps
+        ph = _native.profile_read()
+        _native.profile_enable(False)
+        assert t.n_rows == n
+        k_ms = sum(v[0] for k, v in ph.items() if k.startswith("tsv.")) / reps
+        k_bytes = sum(v[2] for k, v in ph.items() if k.startswith("tsv.")) / reps
+        small = Path(tmp) / "small.tsv"
+        m = max(1, n // 10)
+        small.write_bytes(b"".join(text.splitlines(keepends=True)[:m]))
+        t0 = time.perf_counter()
+        load_tsv(small, schema)
+        host_s = time.perf_counter() - t0
+    return {"rows": n, "bytes": len(text), "e2e_ms": wall * 1e3,
+            "value": n / wall, "unit": "rows/s (file -> HBM columns)",
+            "kernel_ms": k_ms, "kernel_gbs": k_bytes / (k_ms / 1e3) / 1e9 if k_ms else None,
+            "kernel_hbm_frac": (k_bytes / (k_ms / 1e3) / 1e9 / pk["hbm_gbs"]) if k_ms else None,
+            "cpu_host_parser": {"rows": m, "value": m / host_s, "unit": "rows/s", "cores": 1}}
+
 
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
@@ -356,6 +404,8 @@ def ours_arm(args):
                 "achieved_gbs": by_x / args.steps / (ms_x / 1e3) / 1e9,
                 "hbm_frac": by_x / args.steps / (ms_x / 1e3) / 1e9 / pk["hbm_gbs"]}
         del g_x
+        if not args.no_tsv:
+            extras["load_tsv"] = tsv_extra(src, dst, args, pk)
 
     # ---- end to end through the public API with host buffers ---------------
     e2e = None

@@ -118,6 +118,21 @@ GT_API int gt_graph_edge_table(const gt_graph* g, int64_t* src, int64_t* dst, in
 GT_API int gt_graph_node_table(const gt_graph* g, int64_t* node, int64_t* out_deg,
                                int64_t* in_deg, int out_is_device);
 
+/* ---- TSV ingest (tables.load_tsv, tables.py:246-284) ---- */
+
+/* Number of lines of a headerless TSV held in HBM (universal newlines: "\n",
+ * "\r\n" and a lone "\r" end a line; a final unterminated line counts). */
+GT_API int gt_tsv_count_lines(const uint8_t* d_buf, int64_t nbytes, int64_t* n_lines);
+
+/* Parse an all-int TSV (ASCII) into ncols (<= 16) device int64 columns of
+ * n_lines rows (size them with gt_tsv_count_lines). int() semantics per
+ * field. On a bad line: *err_line = its 0-based index and *err_column = -1
+ * (wrong field count) or the 0-based column of the leftmost bad field; the
+ * first bad line is reported. *overflow = 1 when a value does not fit int64. */
+GT_API int gt_tsv_parse_int64(const uint8_t* d_buf, int64_t nbytes, int ncols,
+                              int64_t* const* d_cols, int64_t* n_lines, int64_t* err_line,
+                              int* err_column, int* overflow);
+
 /* ---- PageRank (algorithms.pagerank, algorithms.py:36-87) --------------- */
 
 /* Damped power iteration, fp64, start 1/N, dangling mass redistributed

@@ -40,6 +40,11 @@ SIGNATURES = {
     "gt_graph_free": (None, [_VP]),
     "gt_pagerank": (ctypes.c_int, [_VP, ctypes.c_double, ctypes.c_int, _VP, ctypes.c_int]),
     "gt_graph_edge_table": (ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int]),
+    "gt_tsv_count_lines": (ctypes.c_int, [_VP, ctypes.c_int64, _I64P]),
+    "gt_tsv_parse_int64": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int,
+                                          ctypes.POINTER(ctypes.c_void_p), _I64P, _I64P,
+                                          ctypes.POINTER(ctypes.c_int),
+                                          ctypes.POINTER(ctypes.c_int)]),
     "gt_graph_node_table": (ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int]),
     "gt_triangles": (ctypes.c_int, [_VP, _I64P]),
     "gt_triangle_orientation": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _I64P]),

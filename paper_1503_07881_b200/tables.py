@@ -136,8 +136,76 @@ class ColumnTable:
         return f"ColumnTable({self.schema!r}, rows={self.n_rows})"
 
 
-def load_tsv(path, schema: Schema) -> ColumnTable:
-    """Headerless TSV, one row per line, fields per schema (tables.py:246-284)."""
+def load_tsv(path, schema: Schema, device=None) -> ColumnTable:
+    """Headerless TSV, one row per line, fields per schema (tables.py:246-284).
+
+    ``device="cuda"`` parses an all-int ASCII file on the GPU (gt_tsv_parse_int64,
+    SURVEY §8f next #2) and returns HBM-resident columns — the same values and
+    the same ParseError / OverflowError as the host parser, which stays the
+    default (``device=None``) and handles str / float columns and non-ASCII
+    text."""
+    if device is not None:
+        return _load_tsv_device(path, schema, device)
+    return _load_tsv_host(path, schema)
+
+
+def _line_bounds(data: np.ndarray, k: int):
+    """Byte range of the k-th line (0-based) under universal newlines."""
+    nl = data == 10
+    cr = data == 13
+    lf_after = np.zeros_like(cr)
+    lf_after[:-1] = nl[1:]
+    ends = np.flatnonzero(nl | (cr & ~lf_after))
+    start = 0 if k == 0 else int(ends[k - 1]) + 1
+    end = int(ends[k]) if k < ends.shape[0] else data.shape[0]
+    if end > start and end < data.shape[0] and data[end] == 10 and data[end - 1] == 13:
+        end -= 1
+    return start, end
+
+
+def _load_tsv_device(path, schema: Schema, device) -> ColumnTable:
+    import ctypes
+
+    import torch
+
+    from . import _native
+
+    types = [t for _, t in schema.columns]
+    data = np.fromfile(path, dtype=np.uint8)
+    if any(t != INT for t in types) or len(types) > 16 or (data.size and data.max() >= 0x80):
+        raise TypeMismatchError("device TSV ingest takes all-int schemas (<= 16 columns) of "
+                                "ASCII text; use device=None for the host parser")
+    dev = torch.device(device)
+    buf = torch.from_numpy(data).to(dev) if data.size else torch.empty(1, dtype=torch.uint8,
+                                                                        device=dev)
+    lib = _native.ensure_init()
+    n_lines = ctypes.c_int64()
+    _native.check(lib.gt_tsv_count_lines(buf.data_ptr(), data.size, ctypes.byref(n_lines)),
+                  "gt_tsv_count_lines")
+    n = int(n_lines.value)
+    cols = [torch.empty(max(n, 1), dtype=torch.int64, device=dev) for _ in types]
+    ptrs = (ctypes.c_void_p * len(cols))(*[c.data_ptr() for c in cols])
+    err_line, err_col, overflow = ctypes.c_int64(), ctypes.c_int(), ctypes.c_int()
+    _native.check(lib.gt_tsv_parse_int64(buf.data_ptr(), data.size, len(cols), ptrs,
+                                         ctypes.byref(n_lines), ctypes.byref(err_line),
+                                         ctypes.byref(err_col), ctypes.byref(overflow)),
+                  "gt_tsv_parse_int64")
+    if err_line.value >= 0:
+        lineno = int(err_line.value) + 1
+        a, b = _line_bounds(data, int(err_line.value))
+        fields = data[a:b].tobytes().decode("ascii").split("\t")
+        if err_col.value < 0:
+            raise ParseError(f"line {lineno}: expected {len(types)} fields, got {len(fields)}",
+                             line=lineno)
+        name = schema.columns[err_col.value][0]
+        raise ParseError(f"line {lineno}, column {name!r}: {fields[err_col.value]!r} is not "
+                         "an integer", line=lineno, column=name)
+    if overflow.value:
+        raise OverflowError("Python int too large to convert to C long")
+    return ColumnTable(schema, [c[:n] for c in cols])
+
+
+def _load_tsv_host(path, schema: Schema) -> ColumnTable:
     n_cols = len(schema)
     raw = [[] for _ in range(n_cols)]
     pool: list[str] = []
