@@ -32,6 +32,7 @@
 #include "radix_sort.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace gtd {
 
@@ -426,10 +427,35 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
     GT_LAUNCH(gtd::pr_tile_rows_kernel, ceil_div(tiles + 1, 256), 256, 0, g->in_off, n, tiles,
               tile_row);
   }
+  // L2 residency for the hot sources: after the relabelling the first
+  // positions of the contrib vector are the high out-degree sources; when the
+  // vector is larger than what L2 keeps on its own, an access-policy window
+  // marks its hot head as persisting for the gathers of each iteration.
+  const size_t contrib_bytes = size_t(n) * 8;
+  size_t window = 0;
+  if (contrib_bytes > ctx().l2_bytes / 2 && !getenv("GT_PR_NO_L2_WINDOW")) {
+    int max_win = 0;
+    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, ctx().device);
+    int persist_max = 0;
+    cudaDeviceGetAttribute(&persist_max, cudaDevAttrMaxPersistingL2CacheSize, ctx().device);
+    window = std::min<size_t>({contrib_bytes, size_t(max_win), size_t(persist_max)});
+    if (window > 0) GT_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, window));
+  }
+  auto set_window = [&](const double* base) {
+    if (window == 0) return;
+    cudaStreamAttrValue attr = {};
+    attr.accessPolicyWindow.base_ptr = const_cast<double*>(base);
+    attr.accessPolicyWindow.num_bytes = window;
+    attr.accessPolicyWindow.hitRatio = 1.0f;
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    GT_CUDA(cudaStreamSetAttribute(ctx().stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+  };
   for (int it = 0; it < iterations; ++it) {
     const int last = it == iterations - 1;
     double* cur = contrib[it & 1];
     double* nxt = contrib[(it + 1) & 1];
+    set_window(cur);
     {
       Phase ph("pr.spmv", 12.0 * e + 8.0 * (n + 1) + 20.0 * n);
       GT_LAUNCH(gtd::pr_spmv_kernel, static_cast<int>(tiles), gtd::PR_THREADS, 0, g->in_off,
@@ -442,6 +468,12 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
                 dang + it, damping, head, tail, tail_row, dpart, score, nxt, last, partials,
                 ticket, dang + it + 1);
     }
+  }
+  if (window) {  // release the persisting lines and the stream's window
+    cudaStreamAttrValue attr = {};
+    attr.accessPolicyWindow.num_bytes = 0;
+    GT_CUDA(cudaStreamSetAttribute(ctx().stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+    GT_CUDA(cudaCtxResetPersistingL2Cache());
   }
   if (!on_device) {
     d2h(scores, score, size_t(n) * 8);
