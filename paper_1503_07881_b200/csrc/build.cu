@@ -60,10 +60,13 @@ __global__ void __launch_bounds__(256) minmax_kernel(const int64_t* __restrict__
 
 // Rank map word: presence bits of 32 consecutive ids + number of present ids
 // below the word (exclusive popcount prefix).
+// The check goes through the non-coherent L1 path: a stale 0 only costs a
+// redundant atomicOr (bits are only ever set), and hub ids — most rows on
+// R-MAT — then skip the L2 atomic entirely.
 __device__ __forceinline__ void mark_present(uint2* __restrict__ words, uint64_t off) {
   unsigned int* p = &words[off >> 5].x;
   const unsigned int bit = 1u << (off & 31);
-  if ((*reinterpret_cast<volatile unsigned int*>(p) & bit) == 0) atomicOr(p, bit);
+  if ((__ldg(p) & bit) == 0) atomicOr(p, bit);
 }
 
 __global__ void __launch_bounds__(256) presence_kernel(const int64_t* __restrict__ src,
