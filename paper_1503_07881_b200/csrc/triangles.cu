@@ -100,94 +100,132 @@ __global__ void __launch_bounds__(256) cand_tile_rows_kernel(const int64_t* __re
 // Edge-parallel pass over the concatenated candidate slots of all rows:
 // deg[row] += candidate slots (the undirected degree, graphs.py:163-167), and
 // one keep bit per slot (keep_bits, 2E bits) for the row-parallel fill.
-// The tile's row offsets are staged in shared memory (cat and out_off; the
-// in-offset is their difference), so the per-slot row search and offset
-// reads stay on chip; the per-slot global loads of all PER slots are issued
-// before any of them is consumed.
+// Per 2048-slot tile, in shared memory: the tile's row offsets (relative to
+// the tile, int32), the slot -> row map (row heads scattered, then a block
+// max-scan: no per-slot search), and the tile's neighbour ids, so the
+// reciprocity test of an in-slot (is its source also in the sorted out-row?)
+// is a shared-memory binary search whenever that out-row lies in the tile.
+// Tiles with more than TC_ROWS_CAP - 2 rows (only possible with isolated
+// nodes) map slots by a global binary search instead.
 __global__ void __launch_bounds__(256) cand_degree_kernel(
     const int64_t* __restrict__ cat, const int64_t* __restrict__ tile_row,
     const int64_t* __restrict__ out_off, const int32_t* __restrict__ out_adj,
     const int32_t* __restrict__ in_adj, int64_t n, int64_t slots, int32_t* __restrict__ deg,
     uint32_t* __restrict__ keep_bits) {
-  constexpr int PER = TC_CAND_TILE / 256;
-  __shared__ int64_t s_cat[TC_ROWS_CAP];
-  __shared__ int64_t s_oo[TC_ROWS_CAP];
-  __shared__ int64_t s_r[2];
-  __shared__ uint32_t s_tile;
+  constexpr int T = TC_CAND_TILE, PER = T / 256;
+  __shared__ int32_t s_c[TC_ROWS_CAP];  // cat[r0 + i] - e0
+  __shared__ int32_t s_o[TC_ROWS_CAP];  // out_off[r0 + i] - out_off[r0]
+  __shared__ __align__(16) int32_t s_row[T];  // slot -> row - r0
+  __shared__ int32_t s_j[T];
+  __shared__ int32_t s_wmax[8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) {
-    const uint32_t t = blockIdx.x;
-    s_tile = t;
-    s_r[0] = tile_row[t];
-    s_r[1] = tile_row[t + 1];  // the row holding the next tile's first slot (or the last slot)
-  }
-  __syncthreads();
-  const int64_t e0 = int64_t(s_tile) * TC_CAND_TILE;
-  const int64_t r0 = s_r[0], r1 = s_r[1];
+  const int64_t e0 = int64_t(blockIdx.x) * T;
+  const int64_t r0 = tile_row[blockIdx.x], r1 = tile_row[blockIdx.x + 1];
+  const int64_t oo0 = out_off[r0];
   const int64_t nr = r1 - r0 + 2;  // rows r0..r1 plus the end offset of r1
   const bool staged = nr <= TC_ROWS_CAP;
+  const int tn = int(slots - e0 < T ? slots - e0 : int64_t(T));
   if (staged) {
     for (int i = tid; i < int(nr); i += 256) {
-      s_cat[i] = cat[r0 + i];
-      s_oo[i] = out_off[r0 + i];
+      s_c[i] = int32_t(cat[r0 + i] - e0);
+      s_o[i] = int32_t(out_off[r0 + i] - oo0);
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) s_row[q * 256 + tid] = 0;
+    __syncthreads();
+    // heads of the non-empty rows that start inside the tile (distinct slots)
+    for (int i = tid + 1; i < int(nr) - 1; i += 256) {
+      const int32_t c = s_c[i];
+      if (c < T && s_c[i + 1] > c) s_row[c] = i;
+    }
+    __syncthreads();
+    // inclusive max-scan: thread t owns slots [8t, 8t+8)
+    int4 a = reinterpret_cast<int4*>(s_row)[2 * tid];
+    int4 b = reinterpret_cast<int4*>(s_row)[2 * tid + 1];
+    a.y = max(a.y, a.x); a.z = max(a.z, a.y); a.w = max(a.w, a.z);
+    b.x = max(b.x, a.w); b.y = max(b.y, b.x); b.z = max(b.z, b.y); b.w = max(b.w, b.z);
+    int run = b.w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, run, o);
+      if (lane >= o) run = max(run, y);
+    }
+    if (lane == 31) s_wmax[warp] = run;
+    int excl = __shfl_up_sync(0xffffffffu, run, 1);
+    if (lane == 0) excl = 0;
+    __syncthreads();
+    for (int w = 0; w < warp; ++w) excl = max(excl, s_wmax[w]);
+    a.x = max(a.x, excl); a.y = max(a.y, excl); a.z = max(a.z, excl); a.w = max(a.w, excl);
+    b.x = max(b.x, excl); b.y = max(b.y, excl); b.z = max(b.z, excl); b.w = max(b.w, excl);
+    reinterpret_cast<int4*>(s_row)[2 * tid] = a;
+    reinterpret_cast<int4*>(s_row)[2 * tid + 1] = b;
+  } else {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int t = q * 256 + tid;
+      if (t < tn) s_row[t] = int32_t(row_of(cat, r0, r1, e0 + t) - r0);
     }
   }
   __syncthreads();
-  auto cat_at = [&](int64_t r) { return staged ? s_cat[r - r0] : cat[r]; };
-  auto oo_at = [&](int64_t r) { return staged ? s_oo[r - r0] : out_off[r]; };
+  // row start (tile-relative slot) and out-row extent of relative row ri
+  auto c_at = [&](int ri) -> int64_t { return staged ? s_c[ri] : cat[r0 + ri] - e0; };
+  auto o_at = [&](int ri) -> int64_t { return staged ? s_o[ri] : out_off[r0 + ri] - oo0; };
 
-  // ---- per-slot values (no warp-collective operations: loads overlap) ----
-  int64_t row[PER];
+  // ---- neighbour ids of the tile (all loads issued before any is consumed) ----
   int32_t j[PER];
-  bool cand[PER];
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
-    const int64_t e = e0 + int64_t(warp) * 32 * PER + q * 32 + lane;
-    row[q] = -1;
+    const int t = q * 256 + tid;
     j[q] = 0;
-    cand[q] = false;
-    if (e < slots) {
-      int64_t lo = r0, hi = r1;  // largest r with cat(r) <= e
-      while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (cat_at(mid) <= e) lo = mid;
-        else hi = mid - 1;
-      }
-      const int64_t c = cat_at(lo), oa = oo_at(lo), no = oo_at(lo + 1) - oa;
-      const int64_t k = e - c;
-      row[q] = lo;
-      cand[q] = true;
-      j[q] = k < no ? out_adj[oa + k] : in_adj[(c - oa) + (k - no)];  // in_off = cat - out_off
+    if (t < tn) {
+      const int ri = s_row[t];
+      const int64_t c = c_at(ri), oa = o_at(ri), no = o_at(ri + 1) - oa;
+      const int64_t k = t - c;
+      j[q] = k < no ? out_adj[oo0 + oa + k] : in_adj[(e0 + c) - (oo0 + oa) + (k - no)];
     }
   }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) s_j[q * 256 + tid] = j[q];
+  __syncthreads();
+
   // drop self-loops and in-slots whose source is also an out-neighbour
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
-    if (!cand[q]) continue;
-    const int64_t r = row[q];
-    cand[q] = j[q] != int32_t(r);
-    const int64_t e = e0 + int64_t(warp) * 32 * PER + q * 32 + lane;
-    const int64_t oa = oo_at(r), no = oo_at(r + 1) - oa;
-    if (cand[q] && e - cat_at(r) >= no) cand[q] = !bsearch_in(out_adj + oa, no, j[q]);
-  }
-
-  // per-row counts: the 32 slots of a warp step are consecutive, so each row
-  // is a run of lanes; the first lane of a run adds the run's kept count
-#pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    const bool valid = row[q] >= 0;
+    const int t = q * 256 + tid;
+    const bool valid = t < tn;
+    bool cand = false;
+    int ri = -1;
+    if (valid) {
+      ri = s_row[t];
+      cand = int64_t(j[q]) != r0 + ri;
+      const int64_t c = c_at(ri), oa = o_at(ri), no = o_at(ri + 1) - oa;
+      if (cand && t - c >= no) {
+        if (c >= 0) {  // the whole out-row [c, c+no) precedes t inside the tile
+          int lo = int(c), hi = int(c + no);
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (s_j[mid] < j[q]) lo = mid + 1;
+            else hi = mid;
+          }
+          cand = !(lo < int(c + no) && s_j[lo] == j[q]);
+        } else {
+          cand = !bsearch_in(out_adj + oo0 + oa, no, j[q]);
+        }
+      }
+    }
+    // per-row counts: the 32 slots of a warp step are consecutive, so each
+    // row is a run of lanes; the first lane of a run adds the run's count
     const unsigned active = __ballot_sync(0xffffffffu, valid);
-    const unsigned kb = __ballot_sync(0xffffffffu, cand[q]);
-    if (lane == 0 && active) keep_bits[(e0 + int64_t(warp) * 32 * PER + q * 32) >> 5] = kb;
-    const int32_t r32 = int32_t(row[q]);
-    const int32_t prev = __shfl_up_sync(0xffffffffu, r32, 1);
-    const bool head = valid && (lane == 0 || prev != r32);
+    const unsigned kb = __ballot_sync(0xffffffffu, cand);
+    if (lane == 0 && active) keep_bits[(e0 + q * 256 + warp * 32) >> 5] = kb;
+    const int prev = __shfl_up_sync(0xffffffffu, ri, 1);
+    const bool head = valid && (lane == 0 || prev != ri);
     const unsigned heads = __ballot_sync(0xffffffffu, head);
     if (head) {
       const unsigned after = heads & ~((2u << lane) - 1u);  // later heads
-      const unsigned run = (after ? (after & (0u - after)) - 1u : 0xffffffffu) & ~((1u << lane) - 1u);
-      const int c = __popc(kb & run);
-      if (c) atomicAdd(&deg[row[q]], c);
+      const unsigned runm = (after ? (after & (0u - after)) - 1u : 0xffffffffu) & ~((1u << lane) - 1u);
+      const int cnt = __popc(kb & runm);
+      if (cnt) atomicAdd(&deg[r0 + ri], cnt);
     }
   }
 }
