@@ -283,6 +283,21 @@ constexpr int TC_FILL_BIG = 4096;
 constexpr int TC_SORT_WARP = 1024;
 constexpr int TC_SORT_CTA = 16384;
 
+__device__ __forceinline__ uint64_t warp_bitonic32_u64(uint64_t x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t y = __shfl_xor_sync(0xffffffffu, x, j);
+      const bool up = (lane & k) == 0;
+      const bool lower = (lane & j) == 0;
+      x = ((lower == up) == (y < x)) ? y : x;
+    }
+  }
+  return x;
+}
+
 __device__ __forceinline__ int32_t warp_bitonic32(int32_t x) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -393,6 +408,15 @@ __device__ __forceinline__ bool slot_kept(const uint32_t* __restrict__ bits, int
   return (__ldg(bits + (slot >> 5)) >> (slot & 31)) & 1u;
 }
 
+__device__ __forceinline__ int64_t shfl64(int64_t v, int src) {
+  return static_cast<int64_t>(__shfl_sync(0xffffffffu, static_cast<long long>(v), src));
+}
+
+// Warp per batch of 32 consecutive id-rows: the rows' offsets, rank and slot
+// base are loaded once, coalesced (lane l holding row base+l), and broadcast
+// by shuffle (measured faster than interleaving the rows across warps).
+// Rows with at most 32 candidates are packed several to a warp step (below);
+// longer rows take the warp one at a time.
 __global__ void __launch_bounds__(256) fill_rows_kernel(
     const int64_t* __restrict__ cat, const int64_t* __restrict__ out_off,
     const int32_t* __restrict__ out_adj, const int64_t* __restrict__ in_off,
@@ -404,54 +428,116 @@ __global__ void __launch_bounds__(256) fill_rows_kernel(
   __shared__ uint32_t s_hist[8][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
+  const int64_t nbatch = (n + 31) >> 5;
   const int64_t nwarps = int64_t(gridDim.x) * 8;
-  for (int64_t i = int64_t(blockIdx.x) * 8 + warp; i < n; i += nwarps) {
-    const int64_t oo = out_off[i], no = out_off[i + 1] - oo;
-    const int64_t io = in_off[i], ni = in_off[i + 1] - io;
-    const int64_t total = no + ni;
-    if (total > TC_FILL_BIG) {
-      if (lane == 0) big_fill[atomicAdd(&nbig[0], 1u)] = int32_t(i);
-      continue;
+  for (int64_t bt = int64_t(blockIdx.x) * 8 + warp; bt < nbatch; bt += nwarps) {
+    const int64_t base = bt << 5;
+    const int64_t me = base + lane;
+    int64_t m_oo = 0, m_io = 0, m_c = 0, m_uo = 0;
+    int32_t m_no = 0, m_tot = -1, m_r = 0;
+    if (me < n) {
+      m_oo = out_off[me];
+      m_io = in_off[me];
+      const int64_t no = out_off[me + 1] - m_oo, ni = in_off[me + 1] - m_io;
+      m_c = cat[me];
+      m_uo = und_off[me];
+      m_r = rank[me];
+      m_no = int32_t(no);
+      m_tot = no + ni > TC_FILL_BIG ? -1 : int32_t(no + ni);
+      if (no + ni > TC_FILL_BIG) big_fill[atomicAdd(&nbig[0], 1u)] = int32_t(me);
     }
-    const int32_t ri = rank[i];
-    const int64_t c = cat[i];
-    int32_t* row = buf + und_off[i];
-    int cnt = 0;
-    for (int64_t k0 = 0; k0 < total; k0 += 128) {  // 4 x 32 candidates in flight
-      int32_t val[4];
-      bool keep[4];
+    // rows with 1..32 candidates, packed: the next rows (in lane order) whose
+    // candidates fit in 32 lanes share one step — element -> row by a shuffle
+    // binary search over the packed prefix, survivors sorted by (row, rank)
+    // in one 64-bit shuffle bitonic, each landing at its index in its row
+    if (me < n && m_tot == 0) dplus[me] = 0;
+    unsigned todo = __ballot_sync(0xffffffffu, m_tot > 0 && m_tot <= 32);
+    while (todo) {
+      const bool in = (todo >> lane) & 1u;
+      int inc = in ? m_tot : 0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t k = k0 + 32 * u + lane;
-        keep[u] = k < total && slot_kept(keep_bits, c + k);
-        val[u] = keep[u] ? (k < no ? out_adj[oo + k] : in_adj[io + (k - no)]) : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
       }
+      const int ex = inc - (in ? m_tot : 0);
+      const bool take = in && inc <= 32;
+      todo &= ~__ballot_sync(0xffffffffu, take);
+      const int G = __reduce_max_sync(0xffffffffu, take ? unsigned(inc) : 0u);
+      int k = 0;  // the last lane whose packed prefix is <= lane: this element's row
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (keep[u]) {
-          val[u] = rank[val[u]];
-          keep[u] = val[u] > ri;
+      for (int st = 16; st > 0; st >>= 1)
+        if (__shfl_sync(0xffffffffu, ex, k + st) <= lane) k += st;
+      const int t = lane - __shfl_sync(0xffffffffu, ex, k);
+      const int64_t c = shfl64(m_c, k), oo = shfl64(m_oo, k), io = shfl64(m_io, k);
+      const int32_t no = __shfl_sync(0xffffffffu, m_no, k);
+      const int32_t ri = __shfl_sync(0xffffffffu, m_r, k);
+      bool keep = lane < G && slot_kept(keep_bits, c + t);
+      int32_t val = keep ? (t < no ? out_adj[oo + t] : in_adj[io + (t - no)]) : 0;
+      if (keep) {
+        val = rank[val];
+        keep = val > ri;
+      }
+      const unsigned sb = __ballot_sync(0xffffffffu, keep);
+      if (take) {
+        const unsigned rm = (m_tot == 32 ? 0xffffffffu : ((1u << m_tot) - 1u)) << ex;
+        dplus[me] = __popc(sb & rm);
+      }
+      if (sb == 0) continue;
+      uint64_t key = keep ? (uint64_t(k) << 32) | uint32_t(val) : ~0ull;
+      key = warp_bitonic32_u64(key);
+      const bool has = key != ~0ull;
+      const int k2 = has ? int(key >> 32) : 0;
+      const unsigned peers = __match_any_sync(0xffffffffu, uint32_t(key >> 32));
+      const int64_t uo = shfl64(m_uo, k2);
+      if (has) buf[uo + __popc(peers & lt)] = int32_t(uint32_t(key));
+    }
+    const int rows = n - base < 32 ? int(n - base) : 32;
+    for (int k = 0; k < rows; ++k) {
+      const int32_t total = __shfl_sync(0xffffffffu, m_tot, k);
+      if (total <= 32) continue;  // packed above, or chunked by the big-row kernels
+      const int64_t i = base + k;
+      const int64_t oo = shfl64(m_oo, k), io = shfl64(m_io, k), c = shfl64(m_c, k);
+      const int32_t no = __shfl_sync(0xffffffffu, m_no, k);
+      const int32_t ri = __shfl_sync(0xffffffffu, m_r, k);
+      int32_t* row = buf + shfl64(m_uo, k);
+      int cnt = 0;
+      for (int64_t k0 = 0; k0 < total; k0 += 128) {  // 4 x 32 candidates in flight
+        int32_t val[4];
+        bool keep[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t q = k0 + 32 * u + lane;
+          keep[u] = q < total && slot_kept(keep_bits, c + q);
+          val[u] = keep[u] ? (q < no ? out_adj[oo + q] : in_adj[io + (q - no)]) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (keep[u]) {
+            val[u] = rank[val[u]];
+            keep[u] = val[u] > ri;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const unsigned b = __ballot_sync(0xffffffffu, keep[u]);
+          if (keep[u]) row[cnt + __popc(b & lt)] = val[u];
+          cnt += __popc(b);
         }
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const unsigned b = __ballot_sync(0xffffffffu, keep[u]);
-        if (keep[u]) row[cnt + __popc(b & lt)] = val[u];
-        cnt += __popc(b);
+      if (lane == 0) dplus[i] = cnt;
+      __syncwarp();
+      if (cnt <= 32) {
+        int32_t x = lane < cnt ? row[lane] : INT_MAX;
+        x = warp_bitonic32(x);
+        if (lane < cnt) row[lane] = x;
+      } else if (cnt <= TC_SORT_WARP) {
+        warp_radix_sort(row, cnt, s_sort[warp], s_hist[warp], kbits);
+      } else if (lane == 0) {
+        big_sort[atomicAdd(&nbig[1], 1u)] = int32_t(i);
       }
+      __syncwarp();
     }
-    if (lane == 0) dplus[i] = cnt;
-    __syncwarp();
-    if (cnt <= 32) {
-      int32_t x = lane < cnt ? row[lane] : INT_MAX;
-      x = warp_bitonic32(x);
-      if (lane < cnt) row[lane] = x;
-    } else if (cnt <= TC_SORT_WARP) {
-      warp_radix_sort(row, cnt, s_sort[warp], s_hist[warp], kbits);
-    } else if (lane == 0) {
-      big_sort[atomicAdd(&nbig[1], 1u)] = int32_t(i);
-    }
-    __syncwarp();
   }
 }
 
@@ -1082,7 +1168,7 @@ static Oriented orient(const gt_graph* g) {
   GT_CUDA(cudaMemsetAsync(nbig, 0, 8, s));
   {
     Phase ph("tc.orient", 16.0 * (n + 1) * 2 + 4.0 * slots + 8.0 * n + 4.0 * two_m);
-    GT_LAUNCH(gtd::fill_rows_kernel, grid_cap(ceil_div64(n, 8)), 256, 0, cat, g->out_off,
+    GT_LAUNCH(gtd::fill_rows_kernel, grid_cap(ceil_div64(n, 256)), 256, 0, cat, g->out_off,
               g->out_adj, g->in_off, g->in_adj, n, o.rank, keep_bits, und_off, buf, dplus,
               big_fill, big_sort, nbig, o.kbits);
   }
