@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(256) max_i32_kernel(const int32_t* __restrict_
 // Rows with more than TC_FILL_BIG candidates go to fill_rows_big (CTA per
 // row); rows with more than TC_SORT_WARP survivors to sort_rows_big.
 constexpr int TC_FILL_BIG = 4096;
-constexpr int TC_SORT_WARP = 1024;
+constexpr int TC_SORT_WARP = 512;
 constexpr int TC_SORT_CTA = 16384;
 
 __device__ __forceinline__ uint64_t warp_bitonic32_u64(uint64_t x) {
@@ -319,8 +319,9 @@ template <typename Sync>
 __device__ __forceinline__ void bitonic_smem(int32_t* s, int p, int t0, int nthreads, Sync sync) {
   for (int k = 2; k <= p; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
+      const int lj = __ffs(j) - 1;  // j is a power of two: no integer division
       for (int t = t0; t < p / 2; t += nthreads) {
-        const int e = (t / j) * 2 * j + (t % j);
+        const int e = ((t >> lj) << (lj + 1)) + (t & (j - 1));
         const int f = e + j;
         const bool up = (e & k) == 0;
         const int32_t a = s[e], b = s[f];
@@ -335,15 +336,17 @@ __device__ __forceinline__ void bitonic_smem(int32_t* s, int p, int t0, int nthr
 }
 
 // Stable LSD radix sort (8-bit digits over the low `kbits` bits) of row[0,
-// cnt) by one warp, cnt <= TC_SORT_WARP: ping-pong between the row (global,
-// L1-resident) and a per-warp shared buffer; per pass a shared histogram,
-// its scan, and a rank/scatter in index order (__match_any_sync peers).
-__device__ __forceinline__ void warp_radix_sort(int32_t* row, int cnt, int32_t* sm,
+// cnt) by one warp, cnt <= TC_SORT_WARP: the row is read from global memory
+// once, the passes ping-pong between two per-warp shared buffers, and the
+// sorted row is written back once. Per pass a shared histogram, its scan,
+// and a rank/scatter in index order (__match_any_sync peers).
+__device__ __forceinline__ void warp_radix_sort(int32_t* row, int cnt, int32_t* sa, int32_t* sb,
                                                 uint32_t* hist, int kbits) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
-  int32_t* src = row;
-  int32_t* dst = sm;
+  for (int k = lane; k < cnt; k += 32) sa[k] = row[k];
+  int32_t* src = sa;
+  int32_t* dst = sb;
   for (int shift = 0; shift < kbits; shift += 8) {
 #pragma unroll
     for (int b = lane; b < 256; b += 32) hist[b] = 0u;
@@ -380,10 +383,8 @@ __device__ __forceinline__ void warp_radix_sort(int32_t* row, int cnt, int32_t* 
     src = dst;
     dst = t;
   }
-  if (src != row) {
-    for (int k = lane; k < cnt; k += 32) row[k] = src[k];
-    __syncwarp();
-  }
+  for (int k = lane; k < cnt; k += 32) row[k] = src[k];
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(256) i32_to_u64_kernel(const int32_t* __restrict__ in, int64_t n,
@@ -425,6 +426,7 @@ __global__ void __launch_bounds__(256) fill_rows_kernel(
     int32_t* __restrict__ buf, int32_t* __restrict__ dplus, int32_t* __restrict__ big_fill,
     int32_t* __restrict__ big_sort, unsigned int* __restrict__ nbig, int kbits) {
   __shared__ int32_t s_sort[8][TC_SORT_WARP];
+  __shared__ int32_t s_tmp[8][TC_SORT_WARP];
   __shared__ uint32_t s_hist[8][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
@@ -532,7 +534,7 @@ __global__ void __launch_bounds__(256) fill_rows_kernel(
         x = warp_bitonic32(x);
         if (lane < cnt) row[lane] = x;
       } else if (cnt <= TC_SORT_WARP) {
-        warp_radix_sort(row, cnt, s_sort[warp], s_hist[warp], kbits);
+        warp_radix_sort(row, cnt, s_sort[warp], s_tmp[warp], s_hist[warp], kbits);
       } else if (lane == 0) {
         big_sort[atomicAdd(&nbig[1], 1u)] = int32_t(i);
       }
@@ -619,7 +621,25 @@ __global__ void gather_rows_kernel(const int32_t* __restrict__ rows, int nr,
   if (both) out[nr + r] = a64[i + 1];
 }
 
-// CTA bitonic sort of the rows with 32 < d+ <= TC_SORT_CTA (dynamic smem).
+// Rows with TC_SORT_WARP < d+ <= TC_SORT_MID: warp per row (4 per CTA), the
+// same shared-memory radix sort with larger per-warp buffers (dynamic smem).
+constexpr int TC_SORT_MID = 2048;
+__global__ void __launch_bounds__(128) sort_rows_mid_kernel(const int32_t* __restrict__ rows, int nr,
+                                                            const int64_t* __restrict__ und_off,
+                                                            const int32_t* __restrict__ dplus,
+                                                            int32_t* __restrict__ buf, int kbits) {
+  extern __shared__ int32_t s_dyn[];
+  const int warp = threadIdx.x >> 5;
+  int32_t* sa = s_dyn + warp * (2 * TC_SORT_MID + 256);
+  int32_t* sb = sa + TC_SORT_MID;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sb + TC_SORT_MID);
+  for (int r = blockIdx.x * 4 + warp; r < nr; r += gridDim.x * 4) {
+    const int64_t i = rows[r];
+    warp_radix_sort(buf + und_off[i], dplus[i], sa, sb, hist, kbits);
+  }
+}
+
+// CTA bitonic sort of the rows with TC_SORT_MID < d+ <= TC_SORT_CTA (dynamic smem).
 __global__ void __launch_bounds__(256) sort_rows_big_kernel(const int32_t* __restrict__ rows,
                                                             const int64_t* __restrict__ und_off,
                                                             const int32_t* __restrict__ dplus,
@@ -1232,11 +1252,6 @@ static Oriented orient(const gt_graph* g) {
   }
   if (nb[1]) {
     Phase ph("tc.orient_sort", 0.0);
-    const int smem = gtd::TC_SORT_CTA * 4;
-    GT_CUDA(cudaFuncSetAttribute(gtd::sort_rows_big_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    GT_LAUNCH(gtd::sort_rows_big_kernel, int(nb[1]), 256, smem, big_sort, und_off, dplus, buf);
-    // rows beyond the shared-memory sort: LSD radix sort of that row alone
     const int nr = int(nb[1]);
     int64_t* d_cd = reinterpret_cast<int64_t*>(ws_get(WS_TMP0, size_t(nr) * 16 + 64));
     GT_LAUNCH(gtd::gather_rows_kernel, ceil_div(nr, 256), 256, 0, big_sort, nr,
@@ -1245,7 +1260,38 @@ static Oriented orient(const gt_graph* g) {
               (const int32_t*)nullptr, 0, d_cd + nr);
     std::vector<int64_t> cd(2 * size_t(nr));
     d2h(cd.data(), d_cd, cd.size() * 8);
+    std::vector<int32_t> ids(nr);
+    d2h(ids.data(), big_sort, size_t(nr) * 4);
     sync();
+    // shared-memory bitonic, one launch per padded size so each CTA reserves
+    // only what its rows need; longer rows: LSD radix sort of that row alone
+    std::vector<int32_t> by_size;
+    int32_t* d_rows = big_sort;
+    for (int r = 0; r < nr; ++r)
+      if (cd[r] <= gtd::TC_SORT_MID) by_size.push_back(ids[r]);
+    if (!by_size.empty()) {
+      const int smem = 4 * (2 * gtd::TC_SORT_MID + 256) * 4;
+      GT_CUDA(cudaFuncSetAttribute(gtd::sort_rows_mid_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      h2d(d_rows, by_size.data(), by_size.size() * 4);
+      const int nm_rows = int(by_size.size());
+      GT_LAUNCH(gtd::sort_rows_mid_kernel, std::min(ceil_div(nm_rows, 4), 3 * ctx().sm_count), 128,
+                smem, d_rows, nm_rows, und_off, dplus, buf, o.kbits);
+      d_rows += by_size.size();
+    }
+    for (int p2 = 2 * gtd::TC_SORT_MID; p2 <= gtd::TC_SORT_CTA; p2 <<= 1) {
+      by_size.clear();
+      for (int r = 0; r < nr; ++r)
+        if (cd[r] <= p2 && cd[r] > p2 / 2) by_size.push_back(ids[r]);
+      if (by_size.empty()) continue;
+      h2d(d_rows, by_size.data(), by_size.size() * 4);
+      const int smem = p2 * 4;
+      GT_CUDA(cudaFuncSetAttribute(gtd::sort_rows_big_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      GT_LAUNCH(gtd::sort_rows_big_kernel, int(by_size.size()), 256, smem, d_rows, und_off, dplus,
+                buf);
+      d_rows += by_size.size();
+    }
     for (int r = 0; r < nr; ++r) {
       const int64_t c = cd[r], off = cd[nr + r];
       if (c <= gtd::TC_SORT_CTA) continue;

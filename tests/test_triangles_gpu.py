@@ -115,6 +115,30 @@ def test_hub_orientation_all_table_paths(monkeypatch, window, smem_cap):
     assert gt.triangle_count(build(src, dst)) == want
 
 
+def test_clique_rows_past_the_warp_sorts():
+    """K_2600: oriented rows of every length up to 2599, so the packed (<= 32),
+    warp-radix, mid (warp per row, larger buffers) and CTA-bitonic row sorts
+    all run; every rank-space row must come out strictly ascending."""
+    from paper_1503_07881_b200 import _native
+
+    n = 2600
+    a, b = np.triu_indices(n, 1)
+    rng = np.random.default_rng(17)
+    flip = rng.random(a.shape[0]) < 0.5
+    src = np.where(flip, b, a) * 3 - 1000
+    dst = np.where(flip, a, b) * 3 - 1000
+    dg = build(src, dst)
+    deg, rank, off, adj = _native.triangle_orientation(dg.handle, dg.node_count)
+    assert np.all(deg == n - 1)
+    d = np.diff(off)
+    assert sorted(d.tolist()) == list(range(n))
+    inner = np.ones(adj.shape[0], dtype=bool)
+    starts = off[1:-1]
+    inner[starts[starts < adj.shape[0]]] = False  # a row's first element vs the previous row
+    assert np.all(np.diff(adj)[inner[1:]] > 0)
+    assert gt.triangle_count(dg) == n * (n - 1) * (n - 2) // 6
+
+
 @pytest.mark.parametrize("window", ["64", "1024"])
 def test_small_windows_match_reference_on_rmat(monkeypatch, window):
     from paper_1503_07881_b200.synth import rmat_edges
