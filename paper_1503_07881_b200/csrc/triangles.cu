@@ -446,7 +446,10 @@ __global__ void __launch_bounds__(256) fill_rows_kernel(
       m_r = rank[me];
       m_no = int32_t(no);
       m_tot = no + ni > TC_FILL_BIG ? -1 : int32_t(no + ni);
-      if (no + ni > TC_FILL_BIG) big_fill[atomicAdd(&nbig[0], 1u)] = int32_t(me);
+      if (no + ni > TC_FILL_BIG) {  // hub row: fill_big_kernel, d+ is its cursor
+        dplus[me] = 0;
+        big_fill[atomicAdd(&nbig[0], 1u)] = int32_t(me);
+      }
     }
     // rows with 1..32 candidates, packed: the next rows (in lane order) whose
     // candidates fit in 32 lanes share one step — element -> row by a shuffle
@@ -543,71 +546,80 @@ __global__ void __launch_bounds__(256) fill_rows_kernel(
   }
 }
 
-// Rows with more than TC_FILL_BIG candidates, in chunks of TC_BIG_CHUNK
-// candidates, one CTA each: pass 1 counts the kept candidates of every chunk,
-// the host turns the counts into per-chunk output offsets, pass 2 writes.
-// chunk = (row, index of the chunk inside the row).
+// Rows with more than TC_FILL_BIG candidates (hubs), in chunks of
+// TC_BIG_CHUNK candidates, one pass: a CTA takes a chunk, compacts its
+// survivors and claims their place in the row with one atomicAdd on the row's
+// d+ (zeroed by fill_rows; the row is sorted afterwards, so the order in which
+// chunks land does not matter). Chunks are numbered by a scan of the rows'
+// chunk counts; CTAs stride over them, so the host needs no chunk list.
 constexpr int TC_BIG_CHUNK = 2048;
 
-__device__ __forceinline__ bool big_candidate(const int64_t* __restrict__ cat,
-                                              const int64_t* __restrict__ out_off,
-                                              const int32_t* __restrict__ out_adj,
-                                              const int64_t* __restrict__ in_off,
-                                              const int32_t* __restrict__ in_adj,
-                                              const int32_t* __restrict__ rank,
-                                              const uint32_t* __restrict__ keep_bits, int64_t i,
-                                              int64_t k, int32_t ri, int32_t& val) {
-  const int64_t oo = out_off[i], no = out_off[i + 1] - oo;
-  const int64_t total = no + (in_off[i + 1] - in_off[i]);
-  if (k >= total || !slot_kept(keep_bits, cat[i] + k)) return false;
-  val = rank[k < no ? out_adj[oo + k] : in_adj[in_off[i] + (k - no)]];
-  return val > ri;
+__global__ void __launch_bounds__(256) big_chunk_count_kernel(const int32_t* __restrict__ rows,
+                                                              int nr,
+                                                              const int64_t* __restrict__ cat,
+                                                              int64_t* __restrict__ chunks) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nr) return;
+  const int64_t i = rows[r];
+  chunks[r] = (cat[i + 1] - cat[i] + TC_BIG_CHUNK - 1) / TC_BIG_CHUNK;
 }
 
-__global__ void __launch_bounds__(256) fill_big_count_kernel(
-    const int2* __restrict__ chunks, const int64_t* __restrict__ cat,
-    const int64_t* __restrict__ out_off, const int32_t* __restrict__ out_adj,
-    const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_adj,
-    const int32_t* __restrict__ rank, const uint32_t* __restrict__ keep_bits,
-    int64_t* __restrict__ chunk_cnt) {
-  __shared__ uint32_t s_red[8];
-  const int2 ch = chunks[blockIdx.x];
-  const int64_t i = ch.x;
-  const int32_t ri = rank[i];
-  uint32_t cnt = 0;
-  for (int t = threadIdx.x; t < TC_BIG_CHUNK; t += 256) {
-    int32_t val;
-    cnt += big_candidate(cat, out_off, out_adj, in_off, in_adj, rank, keep_bits, i,
-                         int64_t(ch.y) * TC_BIG_CHUNK + t, ri, val) ? 1u : 0u;
-  }
-  cnt = block_sum_256(cnt, s_red);
-  if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = cnt;
-}
-
-__global__ void __launch_bounds__(256) fill_big_write_kernel(
-    const int2* __restrict__ chunks, const int64_t* __restrict__ chunk_off,
-    const int64_t* __restrict__ row_total, const int64_t* __restrict__ cat,
-    const int64_t* __restrict__ out_off, const int32_t* __restrict__ out_adj,
-    const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_adj,
-    const int32_t* __restrict__ rank, const uint32_t* __restrict__ keep_bits,
-    const int64_t* __restrict__ und_off, int32_t* __restrict__ buf,
-    int32_t* __restrict__ dplus) {
+__global__ void __launch_bounds__(256) fill_big_kernel(
+    const int32_t* __restrict__ rows, int nr, const int64_t* __restrict__ coff,
+    const int64_t* __restrict__ cat, const int64_t* __restrict__ out_off,
+    const int32_t* __restrict__ out_adj, const int64_t* __restrict__ in_off,
+    const int32_t* __restrict__ in_adj, const int32_t* __restrict__ rank,
+    const uint32_t* __restrict__ keep_bits, const int64_t* __restrict__ und_off,
+    int32_t* __restrict__ buf, int32_t* __restrict__ dplus) {
+  constexpr int PER = TC_BIG_CHUNK / 256;
   __shared__ uint32_t s_scan[8];
-  const int2 ch = chunks[blockIdx.x];
-  const int64_t i = ch.x;
-  const int32_t ri = rank[i];
-  int32_t* row = buf + und_off[i] + chunk_off[blockIdx.x];
-  int64_t run = 0;
-  for (int t0 = 0; t0 < TC_BIG_CHUNK; t0 += 256) {
-    int32_t val = 0;
-    const bool keep = big_candidate(cat, out_off, out_adj, in_off, in_adj, rank, keep_bits, i,
-                                    int64_t(ch.y) * TC_BIG_CHUNK + t0 + threadIdx.x, ri, val);
+  __shared__ int32_t s_base;
+  const int64_t nchunks = coff[nr];
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    int lo = 0, hi = nr - 1;  // the row holding chunk ch: last r with coff[r] <= ch
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (coff[mid] <= ch) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t i = rows[lo];
+    const int64_t oo = out_off[i], no = out_off[i + 1] - oo, io = in_off[i];
+    const int64_t c = cat[i], total = cat[i + 1] - c;
+    const int32_t ri = rank[i];
+    const int64_t k0 = (ch - coff[lo]) * TC_BIG_CHUNK;
+    int32_t val[PER];
+    bool keep[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int64_t k = k0 + q * 256 + threadIdx.x;
+      keep[q] = k < total && slot_kept(keep_bits, c + k);
+      val[q] = keep[q] ? (k < no ? out_adj[oo + k] : in_adj[io + (k - no)]) : 0;
+    }
+    uint32_t mine = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      if (keep[q]) {
+        val[q] = rank[val[q]];
+        keep[q] = val[q] > ri;
+      }
+      mine += keep[q] ? 1u : 0u;
+    }
     uint32_t tot;
-    const uint32_t pre = block_excl_scan_256<uint32_t>(keep ? 1u : 0u, s_scan, tot);
-    if (keep) row[run + pre] = val;
-    run += tot;
+    const uint32_t pre = block_excl_scan_256<uint32_t>(mine, s_scan, tot);
+    if (threadIdx.x == 0) s_base = tot ? atomicAdd(&dplus[i], int32_t(tot)) : 0;
+    __syncthreads();
+    int32_t* out = buf + und_off[i] + s_base + pre;
+    __syncthreads();  // s_base is rewritten by the next chunk
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+      if (keep[q]) *out++ = val[q];
   }
-  if (ch.y == 0 && threadIdx.x == 0) dplus[i] = int32_t(row_total[blockIdx.x]);
+}
+
+// Appends rows[0, n) to list[0, n) (the hub rows join the rows to sort).
+__global__ void copy_rows_kernel(const int32_t* __restrict__ rows, int n, int32_t* __restrict__ list) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) list[r] = rows[r];
 }
 
 // out[r] = a[rows[r]] (+ a[rows[r] + 1] into out[nr + r] when `both`).
@@ -1195,60 +1207,17 @@ static Oriented orient(const gt_graph* g) {
   unsigned int nb[2];
   d2h(nb, nbig, sizeof nb);
   sync();
-  if (nb[0]) {  // rows with many candidates: chunked, two passes
+  if (nb[0]) {  // hub rows: chunked, one pass, then sorted with the other long rows
     Phase ph("tc.orient_big", 0.0);
-    std::vector<int32_t> rows(nb[0]);
-    d2h(rows.data(), big_fill, size_t(nb[0]) * 4);
-    sync();
-    std::sort(rows.begin(), rows.end());  // deterministic chunk order
-    h2d(big_fill, rows.data(), rows.size() * 4);
-    int64_t* d_cc = reinterpret_cast<int64_t*>(ws_get(WS_TMP0, rows.size() * 16 + 64));
-    GT_LAUNCH(gtd::gather_rows_kernel, ceil_div(int64_t(rows.size()), 256), 256, 0, big_fill,
-              int(rows.size()), cat, (const int32_t*)nullptr, 1, d_cc);
-    std::vector<int64_t> cc(2 * rows.size());
-    d2h(cc.data(), d_cc, cc.size() * 8);
-    sync();
-    const int64_t* c0 = cc.data();
-    const int64_t* c1 = cc.data() + rows.size();
-    std::vector<int2> chunks;
-    std::vector<size_t> first(rows.size() + 1, 0);
-    for (size_t r = 0; r < rows.size(); ++r) {
-      const int64_t total = c1[r] - c0[r];
-      first[r] = chunks.size();
-      for (int64_t c = 0; c * gtd::TC_BIG_CHUNK < total; ++c)
-        chunks.push_back(make_int2(rows[r], int(c)));
-    }
-    first[rows.size()] = chunks.size();
-    const size_t nc = chunks.size();
-    char* q = static_cast<char*>(ws_get(WS_TMP0, nc * 32 + 256));  // adj_p comes later
-    int2* d_chunks = reinterpret_cast<int2*>(q);
-    int64_t* d_cnt = reinterpret_cast<int64_t*>(d_chunks + nc + 1);
-    int64_t* d_off = d_cnt + nc + 1;
-    int64_t* d_tot = d_off + nc + 1;
-    h2d(d_chunks, chunks.data(), nc * sizeof(int2));
-    GT_LAUNCH(gtd::fill_big_count_kernel, int(nc), 256, 0, d_chunks, cat, g->out_off, g->out_adj,
-              g->in_off, g->in_adj, o.rank, keep_bits, d_cnt);
-    std::vector<int64_t> cnt(nc), off(nc), tot(nc);
-    d2h(cnt.data(), d_cnt, nc * 8);
-    sync();
-    for (size_t r = 0; r < rows.size(); ++r) {
-      int64_t run = 0;
-      for (size_t c = first[r]; c < first[r + 1]; ++c) { off[c] = run; run += cnt[c]; }
-      for (size_t c = first[r]; c < first[r + 1]; ++c) tot[c] = run;
-    }
-    h2d(d_off, off.data(), nc * 8);
-    h2d(d_tot, tot.data(), nc * 8);
-    GT_LAUNCH(gtd::fill_big_write_kernel, int(nc), 256, 0, d_chunks, d_off, d_tot, cat,
+    const int nr = int(nb[0]);
+    int64_t* coff = ws_n<int64_t>(WS_TMP1, size_t(nr) + 1);  // tile_row is dead by now
+    GT_LAUNCH(gtd::big_chunk_count_kernel, ceil_div(nr, 256), 256, 0, big_fill, nr, cat, coff);
+    exclusive_scan_i64(coff, nr, coff + nr);
+    GT_LAUNCH(gtd::fill_big_kernel, 4 * ctx().sm_count, 256, 0, big_fill, nr, coff, cat,
               g->out_off, g->out_adj, g->in_off, g->in_adj, o.rank, keep_bits, und_off, buf,
               dplus);
-    // sort the big rows too: warp-sized ones by the CTA sort below as well
-    std::vector<int32_t> extra;
-    for (size_t r = 0; r < rows.size(); ++r)
-      if (tot[first[r]] > 1) extra.push_back(rows[r]);
-    if (!extra.empty()) {
-      h2d(big_sort + nb[1], extra.data(), extra.size() * 4);
-      nb[1] += unsigned(extra.size());
-    }
+    GT_LAUNCH(gtd::copy_rows_kernel, ceil_div(nr, 256), 256, 0, big_fill, nr, big_sort + nb[1]);
+    nb[1] += nb[0];
   }
   if (nb[1]) {
     Phase ph("tc.orient_sort", 0.0);

@@ -115,13 +115,14 @@ def test_hub_orientation_all_table_paths(monkeypatch, window, smem_cap):
     assert gt.triangle_count(build(src, dst)) == want
 
 
-def test_clique_rows_past_the_warp_sorts():
-    """K_2600: oriented rows of every length up to 2599, so the packed (<= 32),
+@pytest.mark.parametrize("n", [2600, 5000])
+def test_clique_rows_past_the_warp_sorts(n):
+    """K_n: oriented rows of every length up to n-1, so the packed (<= 32),
     warp-radix, mid (warp per row, larger buffers) and CTA-bitonic row sorts
-    all run; every rank-space row must come out strictly ascending."""
+    all run; at n = 5000 every row has more than TC_FILL_BIG candidates (the
+    chunked hub fill). Every rank-space row must come out strictly ascending."""
     from paper_1503_07881_b200 import _native
 
-    n = 2600
     a, b = np.triu_indices(n, 1)
     rng = np.random.default_rng(17)
     flip = rng.random(a.shape[0]) < 0.5
