@@ -633,13 +633,15 @@ __global__ void gather_rows_kernel(const int32_t* __restrict__ rows, int nr,
   if (both) out[nr + r] = a64[i + 1];
 }
 
-// Rows with TC_SORT_WARP < d+ <= TC_SORT_MID: warp per row (4 per CTA), the
-// same shared-memory radix sort with larger per-warp buffers (dynamic smem).
+// Listed rows (d+ > TC_SORT_WARP, and the hub rows) up to TC_SORT_MID: warp
+// per row (4 per CTA), the same shared-memory radix sort with larger per-warp
+// buffers (dynamic smem); longer rows only raise *max_big.
 constexpr int TC_SORT_MID = 2048;
 __global__ void __launch_bounds__(128) sort_rows_mid_kernel(const int32_t* __restrict__ rows, int nr,
                                                             const int64_t* __restrict__ und_off,
                                                             const int32_t* __restrict__ dplus,
-                                                            int32_t* __restrict__ buf, int kbits) {
+                                                            int32_t* __restrict__ buf, int kbits,
+                                                            unsigned int* __restrict__ max_big) {
   extern __shared__ int32_t s_dyn[];
   const int warp = threadIdx.x >> 5;
   int32_t* sa = s_dyn + warp * (2 * TC_SORT_MID + 256);
@@ -647,7 +649,12 @@ __global__ void __launch_bounds__(128) sort_rows_mid_kernel(const int32_t* __res
   uint32_t* hist = reinterpret_cast<uint32_t*>(sb + TC_SORT_MID);
   for (int r = blockIdx.x * 4 + warp; r < nr; r += gridDim.x * 4) {
     const int64_t i = rows[r];
-    warp_radix_sort(buf + und_off[i], dplus[i], sa, sb, hist, kbits);
+    const int cnt = dplus[i];
+    if (cnt > TC_SORT_MID) {  // left to the CTA sorts
+      if ((threadIdx.x & 31) == 0) atomicMax(max_big, unsigned(cnt));
+      continue;
+    }
+    if (cnt > 1) warp_radix_sort(buf + und_off[i], cnt, sa, sb, hist, kbits);
   }
 }
 
@@ -1197,7 +1204,7 @@ static Oriented orient(const gt_graph* g) {
   int32_t* big_fill = lists;
   int32_t* big_sort = lists + n;
   unsigned int* nbig = reinterpret_cast<unsigned int*>(small + 14);
-  GT_CUDA(cudaMemsetAsync(nbig, 0, 8, s));
+  GT_CUDA(cudaMemsetAsync(nbig, 0, 16, s));  // [14] list sizes, [15] max d+ past the warp sorts
   {
     Phase ph("tc.orient", 16.0 * (n + 1) * 2 + 4.0 * slots + 8.0 * n + 4.0 * two_m);
     GT_LAUNCH(gtd::fill_rows_kernel, grid_cap(ceil_div64(n, 256)), 256, 0, cat, g->out_off,
@@ -1219,7 +1226,36 @@ static Oriented orient(const gt_graph* g) {
     GT_LAUNCH(gtd::copy_rows_kernel, ceil_div(nr, 256), 256, 0, big_fill, nr, big_sort + nb[1]);
     nb[1] += nb[0];
   }
+  // long rows (listed in big_sort): warp radix sorts in shared memory; the
+  // rare rows beyond TC_SORT_MID are only flagged here (small[15] = their max
+  // d+) and sorted after the offsets' sync below, so the common case costs no
+  // extra host round trip
   if (nb[1]) {
+    Phase ph("tc.orient_sort", 0.0);
+    const int nr = int(nb[1]);
+    const int smem = 4 * (2 * gtd::TC_SORT_MID + 256) * 4;
+    GT_CUDA(cudaFuncSetAttribute(gtd::sort_rows_mid_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    GT_LAUNCH(gtd::sort_rows_mid_kernel, std::min(ceil_div(nr, 4), 3 * ctx().sm_count), 128, smem,
+              big_sort, nr, und_off, dplus, buf, o.kbits,
+              reinterpret_cast<unsigned int*>(small + 15));
+  }
+  // 4. rank-space offsets of N+ and N-, then rows placed + N- filed
+  {
+    Phase ph("tc.oriented_csr", 8.0 * n + 16.0 * (n + 1) * 2);
+    GT_LAUNCH(gtd::rank_counts_kernel, ceil_div(n, 256), 256, 0, o.rank, o.deg, dplus, n, o.off_p,
+              o.off_m);
+    exclusive_scan_i64(o.off_p, n, small + 4);
+    exclusive_scan_i64(o.off_m, n, small + 5);
+  }
+  int64_t hm[12];
+  d2h(hm, small + 4, sizeof hm);
+  sync();
+  o.m = hm[0];
+  if (uint32_t(hm[11]) > uint32_t(gtd::TC_SORT_MID)) {
+    // rows past the warp sorts: shared-memory bitonic, one launch per padded
+    // size so each CTA reserves only what its rows need; longer rows: LSD
+    // radix sort of that row alone
     Phase ph("tc.orient_sort", 0.0);
     const int nr = int(nb[1]);
     int64_t* d_cd = reinterpret_cast<int64_t*>(ws_get(WS_TMP0, size_t(nr) * 16 + 64));
@@ -1232,22 +1268,8 @@ static Oriented orient(const gt_graph* g) {
     std::vector<int32_t> ids(nr);
     d2h(ids.data(), big_sort, size_t(nr) * 4);
     sync();
-    // shared-memory bitonic, one launch per padded size so each CTA reserves
-    // only what its rows need; longer rows: LSD radix sort of that row alone
     std::vector<int32_t> by_size;
     int32_t* d_rows = big_sort;
-    for (int r = 0; r < nr; ++r)
-      if (cd[r] <= gtd::TC_SORT_MID) by_size.push_back(ids[r]);
-    if (!by_size.empty()) {
-      const int smem = 4 * (2 * gtd::TC_SORT_MID + 256) * 4;
-      GT_CUDA(cudaFuncSetAttribute(gtd::sort_rows_mid_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      h2d(d_rows, by_size.data(), by_size.size() * 4);
-      const int nm_rows = int(by_size.size());
-      GT_LAUNCH(gtd::sort_rows_mid_kernel, std::min(ceil_div(nm_rows, 4), 3 * ctx().sm_count), 128,
-                smem, d_rows, nm_rows, und_off, dplus, buf, o.kbits);
-      d_rows += by_size.size();
-    }
     for (int p2 = 2 * gtd::TC_SORT_MID; p2 <= gtd::TC_SORT_CTA; p2 <<= 1) {
       by_size.clear();
       for (int r = 0; r < nr; ++r)
@@ -1274,16 +1296,6 @@ static Oriented orient(const gt_graph* g) {
       GT_LAUNCH(gtd::u64_to_i32_kernel, ceil_div(c, 256), 256, 0, srt, int64_t(c), buf + off);
     }
   }
-  // 4. rank-space offsets of N+ and N-, then rows placed + N- filed
-  {
-    Phase ph("tc.oriented_csr", 8.0 * n + 16.0 * (n + 1) * 2);
-    GT_LAUNCH(gtd::rank_counts_kernel, ceil_div(n, 256), 256, 0, o.rank, o.deg, dplus, n, o.off_p,
-              o.off_m);
-    exclusive_scan_i64(o.off_p, n, small + 4);
-    exclusive_scan_i64(o.off_m, n, small + 5);
-  }
-  d2h(&o.m, small + 4, 8);
-  sync();
   o.adj_p = ws_n<int32_t>(WS_TMP0, size_t(o.m) + 1);
   o.nm = reinterpret_cast<int2*>(ws_get(WS_TMP1, size_t(o.m) * 8 + 16));
   {
