@@ -845,15 +845,19 @@ __device__ __forceinline__ int tc_log_slots(int64_t d, int cap_log) {
 
 // One warp probes up to 32 suffixes (lane = arc (u,v): positions [s, s+len)
 // of adj, all w > v) against N+(v).
-//  * long suffixes (>= TC_LONG, ~97% of the probes on R-MAT) are walked by
-//    the whole warp one arc at a time, TC_UNROLL coalesced loads in flight;
+//  * long suffixes (>= TC_LONG) are walked by the whole warp one arc at a
+//    time, TC_UNROLL coalesced loads in flight, the next arc prefetched;
 //  * the short rest is flattened: position t of the concatenation of the
 //    short suffixes belongs to the lane whose suffix starts last at or before
 //    t (position -> lane map in shared memory), TC_WIN windows of 32
 //    positions resolved per step, so lanes stay busy and reads coalesced.
-constexpr int TC_WIN = 4;
-constexpr int TC_LONG = 16;
-constexpr int TC_UNROLL = 8;
+// The cost is issued instructions per probe, i.e. lane occupancy: a warp walk
+// of a suffix shorter than 32*TC_UNROLL idles lanes, the flattened walk pays
+// the owner lookup. The three constants were swept on C2
+// (scripts/sweep_tc_consts.sh): 16/4/8 -> 64/7/4 took the count 11.3 -> 8.8 ms.
+constexpr int TC_WIN = 7;
+constexpr int TC_LONG = 64;
+constexpr int TC_UNROLL = 4;
 
 template <typename Probe>
 __device__ __forceinline__ uint32_t tc_wedges32(const int32_t* __restrict__ adj, int2 suffix,
