@@ -38,6 +38,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -743,6 +744,32 @@ __global__ void __launch_bounds__(256) tc_task_count_kernel(const int64_t* __res
   c2[v] = (live && !bm && dp > TC_WARP_MAX) ? (dm + TC_CHUNK_CTA - 1) / TC_CHUNK_CTA : 0;
 }
 
+// Diagnostics (GT_TC_STATS=1): per task kind, the number of v, sum d+(v)
+// (table build work) and the probes (suffix elements) of its N-(v) list.
+__global__ void __launch_bounds__(256) tc_stats_kernel(const int64_t* __restrict__ off_p,
+                                                       const int64_t* __restrict__ off_m,
+                                                       const int2* __restrict__ nm, int64_t n,
+                                                       int64_t bm_bits,
+                                                       unsigned long long* __restrict__ out) {
+  const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int64_t dp = off_p[v + 1] - off_p[v];
+  const int64_t om = off_m[v], dm = off_m[v + 1] - om;
+  if (dp < 1 || dm < 1) return;
+  const int kind = n - 1 - v <= bm_bits ? 0 : dp <= TC_SPLIT_MAX ? 3 : dp <= TC_WARP_MAX ? 1 : 2;
+  unsigned long long pr = 0;
+  for (int64_t j = 0; j < dm; ++j) pr += unsigned(nm[om + j].y);
+  if (kind == 2) {  // CTA tasks by distance from the top: <= 2^17, 2^18, 2^19, 2^20
+    const int64_t dist = n - 1 - v;
+    for (int b = 0; b < 4; ++b)
+      if (dist <= (int64_t(1) << (17 + b))) atomicAdd(&out[16 + b], pr);
+  }
+  atomicAdd(&out[kind * 4 + 0], 1ull);
+  atomicAdd(&out[kind * 4 + 1], (unsigned long long)dp);
+  atomicAdd(&out[kind * 4 + 2], pr);
+  atomicAdd(&out[kind * 4 + 3], (unsigned long long)dm);
+}
+
 __global__ void __launch_bounds__(256) tc_task_fill_kernel(const int64_t* __restrict__ toff,
                                                            int64_t n, int2* __restrict__ tasks) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1044,8 +1071,10 @@ __global__ void __launch_bounds__(256) tc_count_warp_kernel(
   if (lane == 0 && acc) atomicAdd(total, acc);
 }
 
-// Tasks with large d+(v) below the bitmap window, CTA per (v, chunk). N+(v)
-// goes to a hash table as sparse as shared memory allows (TC_CTA_SLOTS slots,
+// Tasks with large d+(v) below the bitmap window, CTA per (v, chunk). When
+// the window (v, n) fits the shared table as a bitmap (2^19 ranks), N+(v) is
+// a CTA bitmap; otherwise it goes to a hash table as sparse as shared memory
+// allows (TC_CTA_SLOTS slots,
 // probed with shared-window loads: nearly every miss resolves in one probe),
 // or, when 2 d+(v) exceeds that, to a per-CTA global table of gtab_slots.
 constexpr int TC_CTA_SLOTS = 1 << 14;  // 64 KB: 3 CTAs per SM
@@ -1070,7 +1099,7 @@ __global__ void __launch_bounds__(256) tc_count_cta_kernel(
     const int64_t* __restrict__ off_p, const int32_t* __restrict__ adj_p,
     const int64_t* __restrict__ off_m, const int2* __restrict__ nm,
     const int2* __restrict__ tasks, int64_t n_tasks, int smem_log, int32_t* __restrict__ gtab,
-    int gtab_log, unsigned long long* __restrict__ total) {
+    int gtab_log, unsigned long long* __restrict__ total, int64_t n, int64_t bm_bits) {
   extern __shared__ __align__(16) int32_t s_cta[];
   __shared__ uint8_t s_start[8][32 * TC_WIN];
   __shared__ unsigned long long s_red[8];
@@ -1082,6 +1111,33 @@ __global__ void __launch_bounds__(256) tc_count_cta_kernel(
     const int v = task.x;
     const int64_t ov = off_p[v];
     const int dv = int(off_p[v + 1] - ov);
+    const int64_t om = off_m[v];
+    const int dm = int(off_m[v + 1] - om);
+    const int begin = task.y * TC_CHUNK_CTA;
+    const int end = min(dm, begin + TC_CHUNK_CTA);
+    if (n - 1 - v <= bm_bits) {
+      // the whole window (v, n) fits a CTA bitmap (the shared table as bits):
+      // one LDS per probe instead of a hash walk (99.6% of these probes at C4)
+      uint32_t* bm = reinterpret_cast<uint32_t*>(s_cta);
+      const int nwords = int((n - 1 - v + 31) >> 5);
+      __syncthreads();  // previous task done with the table
+      for (int i = threadIdx.x; i < nwords; i += 256) bm[i] = 0u;
+      __syncthreads();
+      for (int i = threadIdx.x; i < dv; i += 256) {
+        const uint32_t b = uint32_t(adj_p[ov + i] - v - 1);
+        atomicOr(&bm[b >> 5], 1u << (b & 31));
+      }
+      __syncthreads();
+      const BitmapProbe probe{uint32_t(__cvta_generic_to_shared(bm)), v + 1};
+      uint32_t cnt = 0;
+      for (int jb = begin + warp * 32; jb < end; jb += 256) {
+        const int jj = jb + lane;
+        const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
+        cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
+      }
+      acc += cnt;
+      continue;
+    }
     const bool in_smem = 2 * int64_t(dv) <= (int64_t(1) << smem_log);
     const int log_slots = in_smem ? smem_log : gtab_log;
     int32_t* tab = in_smem ? s_cta : mytab;
@@ -1092,10 +1148,6 @@ __global__ void __launch_bounds__(256) tc_count_cta_kernel(
     const HashProbe ins{tab, uint32_t(slots - 1), log_slots};
     for (int i = threadIdx.x; i < dv; i += 256) ins.insert(adj_p[ov + i]);
     __syncthreads();
-    const int64_t om = off_m[v];
-    const int dm = int(off_m[v + 1] - om);
-    const int begin = task.y * TC_CHUNK_CTA;
-    const int end = min(dm, begin + TC_CHUNK_CTA);
     uint32_t cnt = 0;
     if (in_smem) {
       const SmemHashProbe probe{uint32_t(__cvta_generic_to_shared(tab)), uint32_t(slots - 1),
@@ -1372,6 +1424,23 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
   int64_t h[8];
   d2h(h, small + 8, sizeof h);  // bitmap / warp / CTA task counts, ..., max d+, probes
   sync();
+  if (const char* st = getenv("GT_TC_STATS"); st && atoi(st)) {
+    unsigned long long* d_st = reinterpret_cast<unsigned long long*>(counters + 32);
+    d_st = reinterpret_cast<unsigned long long*>(ws_get(WS_TMP4, 32 * 8));
+    GT_CUDA(cudaMemsetAsync(d_st, 0, 32 * 8, s));
+    GT_LAUNCH(gtd::tc_stats_kernel, ceil_div(n, 256), 256, 0, o.off_p, off_m, nm, n, bm_bits, d_st);
+    unsigned long long hs[32];
+    d2h(hs, d_st, sizeof hs);
+    sync();
+    const char* names[4] = {"bitmap", "hash-warp", "cta", "split"};
+    for (int k = 0; k < 4; ++k)
+      fprintf(stderr, "[gt tc stats] %-9s v=%llu sum_d+=%llu sum_d-=%llu probes=%llu\n", names[k],
+              hs[4 * k], hs[4 * k + 1], hs[4 * k + 3], hs[4 * k + 2]);
+    fprintf(stderr, "[gt tc stats] cta probes with n-1-v <= 2^17..2^20: %llu %llu %llu %llu\n",
+            hs[16], hs[17], hs[18], hs[19]);
+    fprintf(stderr, "[gt tc stats] n=%lld m=%lld max_d+=%lld probes=%lld\n", (long long)n,
+            (long long)m, (long long)h[6], (long long)h[7]);
+  }
   const int64_t n_bm = h[0], n_hw = h[1], n_ct = h[2], n_sp = h[3], max_dp = h[6], probes = h[7];
   const int64_t n_wt = n_sp + n_hw;  // warp tasks after the bitmap ones: split, then hash
   if (n_bm + n_wt + n_ct >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangle work list too long");
@@ -1410,6 +1479,14 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
     const int smem = 4 << smem_log;
     GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_cta_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    // CTA bitmap window = the shared table as bits; a GT_TC_WINDOW test run
+    // turns it off unless GT_TC_CTA_WINDOW (ranks) sets it, so that the hash
+    // paths stay covered
+    int64_t cta_bm_bits = int64_t(smem) * 8;
+    if (getenv("GT_TC_WINDOW")) {
+      const char* cw = getenv("GT_TC_CTA_WINDOW");
+      cta_bm_bits = cw ? std::min<int64_t>(cta_bm_bits, atoll(cw)) : 0;
+    }
     const int grid = static_cast<int>(std::min<int64_t>(n_ct, 3LL * ctx().sm_count));
     int32_t* gtab = nullptr;
     int gtab_log = 0;
@@ -1419,7 +1496,7 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
       gtab = ws_n<int32_t>(WS_TMP4, size_t(grid) << gtab_log);
     }
     GT_LAUNCH(gtd::tc_count_cta_kernel, grid, 256, smem, o.off_p, o.adj_p, off_m, nm,
-              tasks + n_bm + n_wt, n_ct, smem_log, gtab, gtab_log, total);
+              tasks + n_bm + n_wt, n_ct, smem_log, gtab, gtab_log, total, n, cta_bm_bits);
   }
   int64_t result = 0;
   d2h(&result, total, 8);

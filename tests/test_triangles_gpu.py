@@ -95,16 +95,21 @@ def test_c3_full_vs_oracle():
     assert gt.triangle_count(g) == want
 
 
-@pytest.mark.parametrize("window,smem_cap", [(None, None), ("64", None), ("64", "1024"),
-                                             ("256", None)])
-def test_hub_orientation_all_table_paths(monkeypatch, window, smem_cap):
+@pytest.mark.parametrize("window,smem_cap,cta_window", [
+    (None, None, None), ("64", None, None), ("64", "1024", None), ("256", None, None),
+    ("64", None, "1024"), ("64", None, "700")])
+def test_hub_orientation_all_table_paths(monkeypatch, window, smem_cap, cta_window):
     """K_n with n = 1200: oriented out-degrees 0..1199. GT_TC_WINDOW shrinks
     the bitmap window so that the split (bitmap + hash), warp-hash and CTA
-    paths all run; GT_TC_TABLE_SMEM_MAX forces the CTA path's global table."""
+    paths all run; GT_TC_TABLE_SMEM_MAX forces the CTA path's global table;
+    GT_TC_CTA_WINDOW turns on the CTA bitmap for the CTA tasks within that
+    distance of the top (700: some CTA tasks bitmap, the rest hash)."""
     if window is not None:
         monkeypatch.setenv("GT_TC_WINDOW", window)
     if smem_cap is not None:
         monkeypatch.setenv("GT_TC_TABLE_SMEM_MAX", smem_cap)
+    if cta_window is not None:
+        monkeypatch.setenv("GT_TC_CTA_WINDOW", cta_window)
     n = 1200
     a, b = np.triu_indices(n, 1)
     rng = np.random.default_rng(5)
