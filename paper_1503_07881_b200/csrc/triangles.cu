@@ -49,7 +49,7 @@ constexpr int TC_ROWS_CAP = TC_CAND_TILE + 2;  // staged row offsets per tile
 constexpr int TC_SLOTS = 2048;                 // hash slots per warp (8 KB)
 constexpr int TC_WARP_MAX = TC_SLOTS / 4;      // largest d+(v) of a warp hash task
 constexpr int TC_CHUNK = 256;                  // arcs per warp task
-constexpr int TC_CHUNK_CTA = 1024;             // arcs per CTA task
+constexpr int TC_CHUNK_CTA = 16384;           // arcs per CTA task (swept at C4: 1024 -> 16384 = 219 -> 183 ms)
 constexpr int TC_BM_BITS = TC_SLOTS * 32;      // per-warp bitmap window (same 8 KB region)
 constexpr int TC_SPLIT_TOP = TC_BM_BITS / 2;   // split tables: bitmap of the top 2^15 ranks ...
 constexpr int TC_SPLIT_SLOTS = TC_SLOTS / 2;   // ... + hash of the rest (4 KB each)
@@ -1103,9 +1103,25 @@ __global__ void __launch_bounds__(256) tc_count_cta_kernel(
   extern __shared__ __align__(16) int32_t s_cta[];
   __shared__ uint8_t s_start[8][32 * TC_WIN];
   __shared__ unsigned long long s_red[8];
+  __shared__ int s_next;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int32_t* mytab = gtab ? gtab + (int64_t(blockIdx.x) << gtab_log) : nullptr;
   unsigned long long acc = 0;
+  // the warps draw 32-arc groups of the chunk from a shared counter, so the
+  // CTA's end-of-task barrier waits for at most one group, not a fixed share
+  auto walk = [&](int64_t om, int begin, int end, const auto& probe) {
+    uint32_t cnt = 0;
+    while (true) {
+      int g = 0;
+      if (lane == 0) g = atomicAdd(&s_next, 1);
+      const int jb = begin + 32 * __shfl_sync(0xffffffffu, g, 0);
+      if (jb >= end) break;
+      const int jj = jb + lane;
+      const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
+      cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
+    }
+    acc += cnt;
+  };
   for (int64_t it = blockIdx.x; it < n_tasks; it += gridDim.x) {
     const int2 task = tasks[it];
     const int v = task.x;
@@ -1115,12 +1131,13 @@ __global__ void __launch_bounds__(256) tc_count_cta_kernel(
     const int dm = int(off_m[v + 1] - om);
     const int begin = task.y * TC_CHUNK_CTA;
     const int end = min(dm, begin + TC_CHUNK_CTA);
+    __syncthreads();  // previous task done with the table and the group counter
+    if (threadIdx.x == 0) s_next = 0;
     if (n - 1 - v <= bm_bits) {
       // the whole window (v, n) fits a CTA bitmap (the shared table as bits):
       // one LDS per probe instead of a hash walk (99.6% of these probes at C4)
       uint32_t* bm = reinterpret_cast<uint32_t*>(s_cta);
       const int nwords = int((n - 1 - v + 31) >> 5);
-      __syncthreads();  // previous task done with the table
       for (int i = threadIdx.x; i < nwords; i += 256) bm[i] = 0u;
       __syncthreads();
       for (int i = threadIdx.x; i < dv; i += 256) {
@@ -1128,43 +1145,23 @@ __global__ void __launch_bounds__(256) tc_count_cta_kernel(
         atomicOr(&bm[b >> 5], 1u << (b & 31));
       }
       __syncthreads();
-      const BitmapProbe probe{uint32_t(__cvta_generic_to_shared(bm)), v + 1};
-      uint32_t cnt = 0;
-      for (int jb = begin + warp * 32; jb < end; jb += 256) {
-        const int jj = jb + lane;
-        const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
-        cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
-      }
-      acc += cnt;
+      walk(om, begin, end, BitmapProbe{uint32_t(__cvta_generic_to_shared(bm)), v + 1});
       continue;
     }
     const bool in_smem = 2 * int64_t(dv) <= (int64_t(1) << smem_log);
     const int log_slots = in_smem ? smem_log : gtab_log;
     int32_t* tab = in_smem ? s_cta : mytab;
     const int slots = 1 << log_slots;
-    __syncthreads();  // previous task done with the table
     for (int i = threadIdx.x; i < slots; i += 256) tab[i] = TC_EMPTY;
     __syncthreads();
     const HashProbe ins{tab, uint32_t(slots - 1), log_slots};
     for (int i = threadIdx.x; i < dv; i += 256) ins.insert(adj_p[ov + i]);
     __syncthreads();
-    uint32_t cnt = 0;
-    if (in_smem) {
-      const SmemHashProbe probe{uint32_t(__cvta_generic_to_shared(tab)), uint32_t(slots - 1),
-                                log_slots};
-      for (int jb = begin + warp * 32; jb < end; jb += 256) {
-        const int jj = jb + lane;
-        const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
-        cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
-      }
-    } else {
-      for (int jb = begin + warp * 32; jb < end; jb += 256) {
-        const int jj = jb + lane;
-        const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
-        cnt += tc_wedges32(adj_p, sfx, ins, s_start[warp]);
-      }
-    }
-    acc += cnt;
+    if (in_smem)
+      walk(om, begin, end,
+           SmemHashProbe{uint32_t(__cvta_generic_to_shared(tab)), uint32_t(slots - 1), log_slots});
+    else
+      walk(om, begin, end, ins);
   }
   acc = block_sum_256(acc, s_red);
   if (threadIdx.x == 0 && acc) atomicAdd(total, acc);
