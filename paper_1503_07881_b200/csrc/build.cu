@@ -72,8 +72,28 @@ __device__ __forceinline__ void mark_present(uint2* __restrict__ words, uint64_t
 __global__ void __launch_bounds__(256) presence_kernel(const int64_t* __restrict__ src,
                                                        const int64_t* __restrict__ dst, int64_t n,
                                                        int64_t lo, uint2* __restrict__ words) {
+  // U rows per thread per step: all 2U id loads, then all 2U word checks, are
+  // in flight before the first conditional atomic
+  constexpr int U = 4;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < n; i += U * stride) {
+    uint64_t off[2 * U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      off[2 * u] = uint64_t(ld_stream_s64(src + i + u * stride)) - uint64_t(lo);
+      off[2 * u + 1] = uint64_t(ld_stream_s64(dst + i + u * stride)) - uint64_t(lo);
+    }
+    unsigned int seen[2 * U];
+#pragma unroll
+    for (int u = 0; u < 2 * U; ++u) seen[u] = __ldg(&words[off[u] >> 5].x);
+#pragma unroll
+    for (int u = 0; u < 2 * U; ++u) {
+      const unsigned int bit = 1u << (off[u] & 31);
+      if ((seen[u] & bit) == 0) atomicOr(&words[off[u] >> 5].x, bit);
+    }
+  }
+  for (; i < n; i += stride) {
     mark_present(words, uint64_t(ld_stream_s64(src + i)) - uint64_t(lo));
     mark_present(words, uint64_t(ld_stream_s64(dst + i)) - uint64_t(lo));
   }
