@@ -381,7 +381,7 @@ def ours_arm(args):
     dom_gbs = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
     roofline = {"bound": "hbm", "kernel": dom_name,
                 "achieved": dom_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": dom_gbs / pk["hbm_gbs"], "traffic": None,
+                "frac": dom_gbs / pk["hbm_gbs"], "traffic": ncu_traffic(args.config, dom_name),
                 "bytes_per_launch": dom_bytes / max(dom_cnt, 1),
                 "ms_per_launch": dom_ms / max(dom_cnt, 1), "peak_source": pk["source"],
                 "share_of_step": dom_ms / elapsed_ms}
@@ -496,6 +496,22 @@ def ours_arm(args):
 
         dist.destroy_process_group()
     return 0
+
+
+def ncu_traffic(config, phase):
+    """DRAM bytes (read + write) per launch of the phase's kernel, from the
+    committed `ncu --set full` capture summarised in profiles/ncu_traffic.json
+    (scripts/ncu_traffic.py writes it); None when no capture matches."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            entry = json.load(f).get(config, {}).get(phase)
+    except (OSError, ValueError):
+        return None
+    if not entry:
+        return None
+    return {"bytes_per_launch": entry["dram_bytes"], "kernel": entry["kernel"],
+            "source": entry["source"]}
 
 
 def main():

@@ -780,23 +780,39 @@ __global__ void __launch_bounds__(256) tc_task_fill_kernel(const int64_t* __rest
 
 // max d+ (out[0]) and the probe count sum_u d+(u)(d+(u)-1)/2 (out[1]): every
 // suffix element the count kernels read, i.e. their algorithmic traffic.
-__global__ void __launch_bounds__(256) max_dplus_kernel(const int64_t* __restrict__ off, int64_t n,
-                                                        unsigned long long* __restrict__ out) {
-  unsigned long long mx = 0, pr = 0;
+__global__ void __launch_bounds__(256) max_dplus_kernel(const int64_t* __restrict__ off,
+                                                        const int32_t* __restrict__ adj, int64_t n,
+                                                        int64_t win_lo,
+                                                        unsigned long long* __restrict__ out,
+                                                        unsigned long long* __restrict__ out_bm) {
+  unsigned long long mx = 0, pr = 0, pb = 0;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < n; u += stride) {
-    const unsigned long long d = (unsigned long long)(off[u + 1] - off[u]);
+    const int64_t o = off[u];
+    const unsigned long long d = (unsigned long long)(off[u + 1] - o);
     mx = max(mx, d);
     pr += d * (d - (d > 0)) / 2;
+    // t = elements of N+(u) at or above win_lo (its sorted tail): arcs (u,v)
+    // with v there are bitmap-task arcs and probe t(t-1)/2 window elements
+    int64_t lo = 0, hi = int64_t(d);
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (adj[o + mid] < win_lo) lo = mid + 1;
+      else hi = mid;
+    }
+    const unsigned long long t = d - (unsigned long long)lo;
+    pb += t * (t - (t > 0)) / 2;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     pr += __shfl_xor_sync(0xffffffffu, pr, o);
+    pb += __shfl_xor_sync(0xffffffffu, pb, o);
   }
   if ((threadIdx.x & 31) == 0) {
     if (mx) atomicMax(&out[0], mx);
     if (pr) atomicAdd(&out[1], pr);
+    if (pb) atomicAdd(out_bm, pb);
   }
 }
 
@@ -886,8 +902,8 @@ constexpr int TC_WIN = 7;
 constexpr int TC_LONG = 64;
 constexpr int TC_UNROLL = 4;
 
-template <typename Probe>
-__device__ __forceinline__ uint32_t tc_wedges32(const int32_t* __restrict__ adj, int2 suffix,
+template <typename Probe, typename T = int32_t>
+__device__ __forceinline__ uint32_t tc_wedges32(const T* __restrict__ adj, int2 suffix,
                                                 const Probe& probe,
                                                 uint8_t* s_start /* [32 * TC_WIN] */) {
   const int lane = threadIdx.x & 31;
@@ -895,18 +911,18 @@ __device__ __forceinline__ uint32_t tc_wedges32(const int32_t* __restrict__ adj,
   // ---- long suffixes: warp per arc; the first 32*TC_UNROLL positions of the
   // NEXT arc are loaded before the current one is probed (software pipeline)
   unsigned longs = __ballot_sync(0xffffffffu, suffix.y >= TC_LONG);
-  auto fetch = [&](int i, const int32_t*& b, int& l, int32_t (&w)[TC_UNROLL]) {
+  auto fetch = [&](int i, const T*& b, int& l, int32_t (&w)[TC_UNROLL]) {
     b = adj + __shfl_sync(0xffffffffu, suffix.x, i);
     l = __shfl_sync(0xffffffffu, suffix.y, i);
 #pragma unroll
     for (int q = 0; q < TC_UNROLL; ++q) {
       const int k = 32 * q + lane;
-      w[q] = k < l ? __ldg(b + k) : TC_EMPTY;
+      w[q] = k < l ? int32_t(__ldg(b + k)) : TC_EMPTY;
     }
   };
   if (longs) {
     int32_t wa[TC_UNROLL], wb[TC_UNROLL];
-    const int32_t *ba, *bb = adj;
+    const T *ba, *bb = adj;
     int la, lb = 0;
     int i = __ffs(longs) - 1;
     longs &= longs - 1;
@@ -925,7 +941,7 @@ __device__ __forceinline__ uint32_t tc_wedges32(const int32_t* __restrict__ adj,
 #pragma unroll
         for (int q = 0; q < TC_UNROLL; ++q) {
           const int k = k0 + 32 * q + lane;
-          w[q] = k < la ? __ldg(ba + k) : TC_EMPTY;
+          w[q] = k < la ? int32_t(__ldg(ba + k)) : TC_EMPTY;
         }
 #pragma unroll
         for (int q = 0; q < TC_UNROLL; ++q)
@@ -966,7 +982,7 @@ __device__ __forceinline__ uint32_t tc_wedges32(const int32_t* __restrict__ adj,
       const int64_t o = __shfl_sync(0xffffffffu, ou, owner);
       const int ex = __shfl_sync(0xffffffffu, excl, owner);
       const int t = t0 + 32 * q + lane;
-      if (t < tot) w[q] = __ldg(adj + o + (t - ex));
+      if (t < tot) w[q] = int32_t(__ldg(adj + o + (t - ex)));
     }
 #pragma unroll
     for (int q = 0; q < TC_WIN; ++q)
@@ -974,6 +990,19 @@ __device__ __forceinline__ uint32_t tc_wedges32(const int32_t* __restrict__ adj,
     __syncwarp();
   }
   return cnt;
+}
+
+// Bitmap tasks only read suffix elements w > v inside the window
+// [base16, n) (base16 = n - window), so they read them from adj16, a copy of
+// adj_p holding w - base16 in 16 bits: the same load count, half the bytes
+// and half the L2 footprint of the suffix data.
+__global__ void __launch_bounds__(256) adj16_kernel(const int32_t* __restrict__ adj, int64_t m,
+                                                    int32_t base16, uint16_t* __restrict__ adj16) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t a = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; a < m; a += stride) {
+    const int32_t w = adj[a];
+    adj16[a] = w >= base16 ? uint16_t(w - base16) : uint16_t(0);
+  }
 }
 
 // Warp per task (v, chunk of N-(v)), dynamic task grabbing. Each warp owns
@@ -986,7 +1015,7 @@ __global__ void __launch_bounds__(256) tc_count_warp_kernel(
     const int64_t* __restrict__ off_m, const int2* __restrict__ nm,
     const int2* __restrict__ tasks, int64_t n_bitmap_tasks, int64_t n_split_end, int64_t n_tasks,
     int64_t n, int split_top, int part, int nparts, unsigned int* __restrict__ next_task,
-    unsigned long long* __restrict__ total) {
+    unsigned long long* __restrict__ total, const uint16_t* __restrict__ adj16, int32_t base16) {
   extern __shared__ int32_t s_tab[];  // [8][TC_SLOTS]
   __shared__ uint8_t s_start[8][32 * TC_WIN];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1052,11 +1081,11 @@ __global__ void __launch_bounds__(256) tc_count_warp_kernel(
         cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
       }
     } else if (use_bm) {
-      const BitmapProbe probe{uint32_t(__cvta_generic_to_shared(bm)), v + 1};
+      const BitmapProbe probe{uint32_t(__cvta_generic_to_shared(bm)), v + 1 - base16};
       for (int jb = task.y * TC_CHUNK; jb < end; jb += 32) {
         const int jj = jb + lane;
         const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
-        cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
+        cnt += tc_wedges32(adj16, sfx, probe, s_start[warp]);
       }
     } else {
       for (int jb = task.y * TC_CHUNK; jb < end; jb += 32) {
@@ -1415,8 +1444,11 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
     exclusive_scan_i64(t1, n, small + 9);
     exclusive_scan_i64(t2, n, small + 10);
     exclusive_scan_i64(t3, n, small + 11);
-    GT_LAUNCH(gtd::max_dplus_kernel, grid_cap(ceil_div64(n, 256)), 256, 0, o.off_p, n,
-              reinterpret_cast<unsigned long long*>(small + 14));  // [14] max d+, [15] probes
+    GT_CUDA(cudaMemsetAsync(small + 12, 0, 8, s));
+    GT_LAUNCH(gtd::max_dplus_kernel, grid_cap(ceil_div64(n, 256)), 256, 0, o.off_p, o.adj_p, n,
+              n - 1 - bm_bits, reinterpret_cast<unsigned long long*>(small + 14),
+              reinterpret_cast<unsigned long long*>(small + 12));
+    // [14] max d+, [15] probes, [12] probes of the bitmap tasks
   }
   int64_t h[8];
   d2h(h, small + 8, sizeof h);  // bitmap / warp / CTA task counts, ..., max d+, probes
@@ -1435,10 +1467,11 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
               hs[4 * k], hs[4 * k + 1], hs[4 * k + 3], hs[4 * k + 2]);
     fprintf(stderr, "[gt tc stats] cta probes with n-1-v <= 2^17..2^20: %llu %llu %llu %llu\n",
             hs[16], hs[17], hs[18], hs[19]);
-    fprintf(stderr, "[gt tc stats] n=%lld m=%lld max_d+=%lld probes=%lld\n", (long long)n,
-            (long long)m, (long long)h[6], (long long)h[7]);
+    fprintf(stderr, "[gt tc stats] n=%lld m=%lld max_d+=%lld probes=%lld probes_bm=%lld\n", (long long)n,
+            (long long)m, (long long)h[6], (long long)h[7], (long long)h[4]);
   }
   const int64_t n_bm = h[0], n_hw = h[1], n_ct = h[2], n_sp = h[3], max_dp = h[6], probes = h[7];
+  const int64_t probes_bm = h[4];  // read as 16-bit window ranks (adj16)
   const int64_t n_wt = n_sp + n_hw;  // warp tasks after the bitmap ones: split, then hash
   if (n_bm + n_wt + n_ct >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangle work list too long");
   int2* tasks = ws_n<int2>(WS_TMP2, size_t(n_bm + n_wt + n_ct) + 1);  // buf is dead by now
@@ -1454,16 +1487,22 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
   unsigned long long* total = reinterpret_cast<unsigned long long*>(small + 6);
   GT_CUDA(cudaMemsetAsync(total, 0, 8, s));
   if (n_bm + n_wt) {
-    // algorithmic bytes: every probed suffix element (4 B), the N- entries (8 B)
-    // and the N+ lists loaded into tables (4 B); hash tasks counted here too
-    Phase ph("tc.count", 4.0 * double(probes) + 12.0 * m);
+    // algorithmic bytes: every probed suffix element (2 B for the bitmap
+    // tasks, which read adj16, 4 B otherwise), the N- entries (8 B) and the N+
+    // lists loaded into tables (4 B); hash tasks counted here too
+    Phase ph("tc.count", 2.0 * double(probes_bm) + 4.0 * double(probes - probes_bm) + 12.0 * m);
     GT_CUDA(cudaMemsetAsync(counters + 22, 0, 4, s));
     const int smem = 8 * gtd::TC_SLOTS * 4;
     GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_warp_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    // 16-bit copy of the window ranks for the bitmap tasks
+    const int32_t base16 = int32_t(n - bm_bits);
+    uint16_t* adj16 = reinterpret_cast<uint16_t*>(ws_get(WS_KEYS_A, size_t(m) * 2 + 64));
+    if (n_bm) GT_LAUNCH(gtd::adj16_kernel, grid_cap(ceil_div64(m, 256)), 256, 0, o.adj_p, m, base16,
+                        adj16);
     GT_LAUNCH(gtd::tc_count_warp_kernel, ctx().sm_count * 3, 256, smem, o.off_p, o.adj_p, off_m,
               nm, tasks, n_bm, n_bm + n_sp, n_bm + n_wt, n, split_top, part, nparts, counters + 22,
-              total);
+              total, adj16, base16);
   }
   if (n_ct) {
     Phase ph("tc.count_hash", 0.0);
