@@ -36,6 +36,20 @@
 
 namespace gtd {
 
+// Gathers: the head of contrib (the PR_HOT highest out-degree sources after
+// the relabelling) through the L1-allocating non-coherent path, the tail with
+// L1::no_allocate. Measured (scripts/sweep_const.sh): spmv C2 7.75 -> 7.48 ms,
+// C4 203 -> 172 ms against __ldg for all; the split point itself did not
+// matter (0 .. 2^20 within noise), while a plain no_allocate load for every
+// gather compiled to a slower schedule (C2 10.7 ms).
+constexpr int PR_HOT = 1 << 15;
+__device__ __forceinline__ double pr_gather(const double* contrib, int32_t u) {
+  if (u < PR_HOT) return __ldg(contrib + u);
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(contrib + u));
+  return v;
+}
+
 constexpr int PR_THREADS = 256;
 constexpr int PR_TILE = 2048;
 
@@ -276,7 +290,7 @@ __global__ void __launch_bounds__(PR_THREADS) pr_spmv_kernel(
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const int j = i * PR_THREADS + threadIdx.x;
-    if (j < ne) vals[j] = __ldg(contrib + idx[i]);
+    if (j < ne) vals[j] = pr_gather(contrib, idx[i]);
   }
   __syncthreads();
 
