@@ -201,13 +201,37 @@ def graph_free(handle: int):
         _lib.gt_graph_free(handle)
 
 
+_PINNED_MAX = 1 << 30  # bytes; larger one-off outputs stay pageable
+
+
+def host_empty(n: int, dtype) -> np.ndarray:
+    """Uninitialised host array for a device->host result. Node-sized results
+    (scores, ids) come from torch's caching pinned-host allocator: the copy
+    runs at full link rate into pages that are already mapped, and the block
+    returns to the cache when the array is freed (a pageable buffer costs a
+    staging copy plus first-touch page faults: ~5 ms per 19 MB at C2)."""
+    dtype = np.dtype(dtype)
+    if 0 < n * dtype.itemsize <= _PINNED_MAX:
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.int64): torch.int64,
+                       np.dtype(np.int32): torch.int32}.get(dtype)
+                if tdt is not None:
+                    return torch.empty(n, dtype=tdt, pin_memory=True).numpy()
+        except Exception:
+            pass
+    return np.empty(n, dtype=dtype)
+
+
 def pagerank(handle: int, n: int, damping: float, iterations: int, out_ptr: int | None = None):
     lib = ensure_init()
     if out_ptr is not None:
         check(lib.gt_pagerank(handle, float(damping), int(iterations), int(out_ptr), 1),
               "gt_pagerank")
         return None
-    scores = np.empty(n, dtype=np.float64)
+    scores = host_empty(n, np.float64)
     check(lib.gt_pagerank(handle, float(damping), int(iterations), _ptr(scores), 0),
           "gt_pagerank")
     return scores

@@ -93,7 +93,7 @@ def pagerank(g, damping: float = 0.85, iterations: int = 10,
 
 
 def _ids_only(dg: DeviceGraph) -> np.ndarray:
-    ids = np.empty(dg.node_count, dtype=np.int64)
+    ids = _native.host_empty(dg.node_count, np.int64)
     if ids.size:
         _native.check(_native.load().gt_graph_export(dg.handle, ids.ctypes.data, None, None,
                                                      None, None), "gt_graph_export")
