@@ -13,6 +13,7 @@ namespace gtd {
 using gt::SortPlan;
 
 constexpr int SEG_KPT = 16;
+constexpr int SEG_MIN_CTAS = 4;  // resident CTAs per SM the register budget is sized for
 constexpr int SEG_TILE = 256 * SEG_KPT;
 
 // Warp-cooperative fill of off[first..last] = v for the lanes that own a gap.
@@ -32,7 +33,7 @@ __device__ __forceinline__ void warp_fill_gaps(bool have, int64_t first, int64_t
 // Sorted packed keys -> CSR rows. DEDUPE: drop repeated keys (convert.py:76-80),
 // emit in-keys (dst<<k|src) plus their digit histograms for the in-sort.
 template <bool DEDUPE>
-__global__ void __launch_bounds__(256, 3) segment_kernel(
+__global__ void __launch_bounds__(256, SEG_MIN_CTAS) segment_kernel(
     const uint64_t* __restrict__ keys, int64_t n, int kbits, int64_t n_rows,
     int32_t* __restrict__ adj, int64_t* __restrict__ off, uint64_t* __restrict__ in_keys,
     SortPlan in_plan, unsigned long long* __restrict__ in_hist, uint64_t* __restrict__ status,
