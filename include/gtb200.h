@@ -160,6 +160,28 @@ GT_API int gt_triangles(const gt_graph* g, int64_t* count);
 GT_API int gt_triangle_orientation(const gt_graph* g, int32_t* h_deg, int32_t* h_rank,
                                    int64_t* h_off_p, int32_t* h_adj_p, int64_t* m);
 
+/* ---- other CSR consumers (algorithms.py:122-248) ---- */
+
+/* Hop distances from the node of dense index `source_index` along out-edges
+ * (algorithms.sssp, algorithms.py:125-141): dist[N] int32, -1 = unreachable
+ * (the reference's None); host or device buffer. GT_EINVAL for an index
+ * outside [0, N). */
+GT_API int gt_bfs(const gt_graph* g, int64_t source_index, int32_t* dist, int dist_is_device);
+
+/* Weakly connected components of the symmetrised graph
+ * (algorithms.connected_components, algorithms.py:232-248): labels[N] int64,
+ * dense, numbered in the order of each component's smallest node id (the
+ * reference labels components as it meets them scanning ids ascending);
+ * *n_components (may be NULL) = number of components. */
+GT_API int gt_connected_components(const gt_graph* g, int64_t* labels, int labels_is_device,
+                                   int64_t* n_components);
+
+/* k-core (algorithms.k_core, algorithms.py:206-229): the induced subgraph
+ * (graphs.py:169-183, every original edge between survivors) on the maximal
+ * node set whose members keep >= k distinct undirected neighbours inside it,
+ * as a new graph (free with gt_graph_free). GT_EINVAL for k < 1. */
+GT_API int gt_kcore(const gt_graph* g, int k, gt_graph** out);
+
 /* ---- synthetic inputs (bench / tests; no reference counterpart) --------- */
 
 /* R-MAT edge table generated on the device, bit-identical to the numpy

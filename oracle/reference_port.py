@@ -296,3 +296,97 @@ def triangle_count_fast(g: CSR, threads: int = 0) -> int:
     in_d = np.ascontiguousarray(np.searchsorted(g.ids, g.in_adj), dtype=np.int64)
     return int(lib.oracle_triangles(g.n, np.ascontiguousarray(g.out_off), out_d,
                                     np.ascontiguousarray(g.in_off), in_d, int(threads)))
+
+
+# ------------------------------------- algorithms.py:122-248 (§8f next #4)
+
+def sssp_csr(g: CSR, source_index: int) -> np.ndarray:
+    """algorithms.py:125-141 — BFS over out-edges from the node of dense index
+    source_index; hop counts aligned with g.ids, -1 for unreachable (None)."""
+    from collections import deque
+
+    n = g.n
+    out_d = np.searchsorted(g.ids, g.out_adj)
+    dist = np.full(n, -1, dtype=np.int64)
+    dist[source_index] = 0
+    queue = deque([source_index])
+    while queue:
+        u = queue.popleft()
+        d = dist[u] + 1
+        for v in out_d[g.out_off[u]:g.out_off[u + 1]].tolist():
+            if dist[v] < 0:
+                dist[v] = d
+                queue.append(v)
+    return dist
+
+
+def components_csr(g: CSR, und=None) -> np.ndarray:
+    """algorithms.py:232-248 — BFS over undirected neighbours from every
+    unlabelled node in ascending id order; labels dense in that order."""
+    from collections import deque
+
+    n = g.n
+    if und is None:
+        und = undirected_dense(g)
+    labels = np.full(n, -1, dtype=np.int64)
+    nxt = 0
+    for start in range(n):
+        if labels[start] >= 0:
+            continue
+        labels[start] = nxt
+        queue = deque([start])
+        while queue:
+            u = queue.popleft()
+            for v in und[u].tolist():
+                if labels[v] < 0:
+                    labels[v] = nxt
+                    queue.append(v)
+        nxt += 1
+    return labels
+
+
+def k_core_csr(g: CSR, k: int, und=None) -> CSR:
+    """algorithms.py:206-229 — peel nodes with fewer than k distinct undirected
+    neighbours (queue order), then graphs.py:169-183's induced subgraph on the
+    survivors (every original edge between two survivors)."""
+    from collections import deque
+
+    if k < 1:
+        raise ValueError(f"k must be >= 1, got {k}")
+    n = g.n
+    if und is None:
+        und = undirected_dense(g)
+    deg = np.asarray([u.shape[0] for u in und], dtype=np.int64)
+    alive = np.ones(n, dtype=bool)
+    queue = deque(i for i in range(n) if deg[i] < k)
+    while queue:
+        i = queue.popleft()
+        if not alive[i]:
+            continue
+        alive[i] = False
+        for m in und[i].tolist():
+            if alive[m]:
+                deg[m] -= 1
+                if deg[m] == k - 1:
+                    queue.append(m)
+    out_d = np.searchsorted(g.ids, g.out_adj)
+    src_d = np.repeat(np.arange(n, dtype=np.int64), np.diff(g.out_off))
+    keep = alive[src_d] & alive[out_d] if out_d.size else np.zeros(0, dtype=bool)
+    return build_csr(g.ids[src_d[keep]], g.ids[out_d[keep]], workers=1)
+
+
+def add_isolated(g: CSR, extra) -> CSR:
+    """graphs.py:92-96 (Graph.add_node) on a CSR: the ids in `extra` not yet
+    present become nodes without edges (empty rows at their sorted place)."""
+    extra = np.setdiff1d(np.asarray(extra, dtype=np.int64), g.ids)
+    if extra.size == 0:
+        return g
+    ids = np.union1d(g.ids, extra)
+    pos = np.searchsorted(ids, g.ids)
+    out_deg = np.zeros(ids.size, dtype=np.int64)
+    in_deg = np.zeros(ids.size, dtype=np.int64)
+    out_deg[pos] = np.diff(g.out_off)
+    in_deg[pos] = np.diff(g.in_off)
+    out_off = np.concatenate(([0], np.cumsum(out_deg))).astype(np.int64)
+    in_off = np.concatenate(([0], np.cumsum(in_deg))).astype(np.int64)
+    return CSR(ids, out_off, g.out_adj, in_off, g.in_adj)

@@ -9,7 +9,8 @@ CUDA, C ABI in ``include/gtb200.h``); importing this package never touches
 the GPU, calling the path without the library raises ``NativeError``.
 """
 
-from .algorithms import RankMap, pagerank, pagerank_device, triangle_count
+from .algorithms import (DistMap, LabelMap, RankMap, connected_components, k_core, pagerank,
+                         pagerank_device, sssp, triangle_count)
 from .convert import EdgeSpec, graph_to_edge_table, graph_to_node_table, table_to_graph
 from .errors import (
     CapacityError,
@@ -34,5 +35,6 @@ __all__ = [
     "Schema", "SchemaError", "TypeMismatchError", "UnknownColumnError", "UnknownNodeError",
     "edge_table", "from_edges", "graph_to_edge_table", "graph_to_node_table", "load_tsv",
     "pagerank", "pagerank_device", "save_tsv", "table_from_map", "table_to_graph",
-    "triangle_count", "upload",
+    "triangle_count", "upload", "sssp", "connected_components", "k_core", "DistMap",
+    "LabelMap",
 ]

@@ -48,6 +48,9 @@ SIGNATURES = {
     "gt_graph_node_table": (ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int]),
     "gt_triangles": (ctypes.c_int, [_VP, _I64P]),
     "gt_triangle_orientation": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _I64P]),
+    "gt_bfs": (ctypes.c_int, [_VP, ctypes.c_int64, _VP, ctypes.c_int]),
+    "gt_connected_components": (ctypes.c_int, [_VP, _VP, ctypes.c_int, _I64P]),
+    "gt_kcore": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.POINTER(_VP)]),
     "gt_rmat_generate": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
                                         ctypes.c_int, _VP, _VP]),
@@ -242,6 +245,32 @@ def triangles(handle: int) -> int:
     c = ctypes.c_int64()
     check(lib.gt_triangles(handle, ctypes.byref(c)), "gt_triangles")
     return int(c.value)
+
+
+def bfs(handle: int, n: int, source_index: int) -> np.ndarray:
+    """-> dist[N] int32 (-1 = unreachable)."""
+    lib = ensure_init()
+    dist = host_empty(n, np.int32)
+    check(lib.gt_bfs(handle, int(source_index), _ptr(dist), 0), "gt_bfs")
+    return dist
+
+
+def connected_components(handle: int, n: int):
+    """-> (labels[N] int64, number of components)."""
+    lib = ensure_init()
+    labels = host_empty(n, np.int64)
+    count = ctypes.c_int64()
+    check(lib.gt_connected_components(handle, _ptr(labels) if n else None, 0, ctypes.byref(count)),
+          "gt_connected_components")
+    return labels, int(count.value)
+
+
+def kcore(handle: int, k: int) -> int:
+    """-> handle of the k-core graph (caller owns it)."""
+    lib = ensure_init()
+    out = _VP()
+    check(lib.gt_kcore(handle, int(k), ctypes.byref(out)), "gt_kcore")
+    return out.value or 0
 
 
 def triangle_orientation(handle: int, n: int):

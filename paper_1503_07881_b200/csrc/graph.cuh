@@ -24,6 +24,14 @@ struct gt_graph {
 };
 
 namespace gt {
+// Undirected degree |out(i) ∪ in(i) \ {i}| of every node (graphs.py:163-167)
+// into deg[N], cat[N+1] = out_off + in_off (offsets of the concatenated
+// out(i) ++ in(i) candidate slots) and one keep bit per slot (a slot is an
+// undirected neighbour unless it is a self-loop or an in-slot whose source is
+// also in the out-row): returned, valid until the next call that uses the
+// WS_RANKMAP workspace slot (triangles.cu).
+uint32_t* undirected_degrees(const gt_graph* g, int64_t* cat, int32_t* deg, const char* phase);
+
 inline int bits_for(int64_t n) {  // bits needed to hold values 0..n-1 (>= 1)
   int b = 1;
   while (b < 63 && (int64_t(1) << b) < n) ++b;

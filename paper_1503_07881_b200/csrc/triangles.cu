@@ -1204,6 +1204,24 @@ static int grid_cap(int64_t blocks) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, 8LL * ctx().sm_count)));
 }
 
+uint32_t* undirected_degrees(const gt_graph* g, int64_t* cat, int32_t* deg, const char* phase) {
+  const int64_t n = g->n, slots = 2 * g->e;
+  cudaStream_t s = ctx().stream;
+  const int64_t tiles = ceil_div64(slots, gtd::TC_CAND_TILE);
+  if (tiles >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "undirected degrees: too many slot tiles");
+  GT_CUDA(cudaMemsetAsync(deg, 0, size_t(n) * 4, s));
+  int64_t* tile_row = ws_n<int64_t>(WS_TMP1, size_t(tiles) + 1);
+  uint32_t* keep_bits = ws_n<uint32_t>(WS_RANKMAP, size_t(tiles) * (gtd::TC_CAND_TILE / 32));
+  Phase ph(phase, 8.0 * (n + 1) * 3 + 4.0 * slots + 4.0 * n + slots / 8.0);
+  GT_LAUNCH(gtd::cat_off_kernel, ceil_div(n + 1, 256), 256, 0, g->out_off, g->in_off, n, cat);
+  if (tiles == 0) return keep_bits;
+  GT_LAUNCH(gtd::cand_tile_rows_kernel, ceil_div(tiles + 1, 256), 256, 0, cat, n, slots, tiles,
+            tile_row);
+  GT_LAUNCH(gtd::cand_degree_kernel, static_cast<int>(tiles), 256, 0, cat, tile_row, g->out_off,
+            g->out_adj, g->in_adj, n, slots, deg, keep_bits);
+  return keep_bits;
+}
+
 // Degree-ordered orientation in rank space (device scratch, valid until the
 // next library call that uses the workspace).
 struct Oriented {
@@ -1239,21 +1257,11 @@ static Oriented orient(const gt_graph* g) {
   unsigned int* cur = reinterpret_cast<unsigned int*>(carve(size_t(n) * 4));
   int32_t* order = reinterpret_cast<int32_t*>(carve(size_t(n) * 4));
 
-  const int64_t tiles = ceil_div64(slots, gtd::TC_CAND_TILE);
-  if (tiles >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangles: too many slot tiles");
-  const double cand_bytes = 8.0 * (n + 1) * 3 + 4.0 * slots + 4.0 * n;
   // 1. undirected degrees over the concatenated (out ++ in) rows
-  GT_CUDA(cudaMemsetAsync(o.deg, 0, size_t(n) * 4, s));
   GT_CUDA(cudaMemsetAsync(small + 12, 0, 8, s));
-  int64_t* tile_row = ws_n<int64_t>(WS_TMP1, size_t(tiles) + 1);
-  uint32_t* keep_bits = ws_n<uint32_t>(WS_RANKMAP, size_t(tiles) * (gtd::TC_CAND_TILE / 32));
+  uint32_t* keep_bits = undirected_degrees(g, cat, o.deg, "tc.und_degree");
   {
-    Phase ph("tc.und_degree", cand_bytes + slots / 8.0);
-    GT_LAUNCH(gtd::cat_off_kernel, ceil_div(n + 1, 256), 256, 0, g->out_off, g->in_off, n, cat);
-    GT_LAUNCH(gtd::cand_tile_rows_kernel, ceil_div(tiles + 1, 256), 256, 0, cat, n, slots, tiles,
-              tile_row);
-    GT_LAUNCH(gtd::cand_degree_kernel, static_cast<int>(tiles), 256, 0, cat, tile_row,
-              g->out_off, g->out_adj, g->in_adj, n, slots, o.deg, keep_bits);
+    Phase ph("tc.und_degree", 0.0);
     GT_LAUNCH(gtd::max_i32_kernel, grid_cap(ceil_div64(n, 256)), 256, 0, o.deg, n,
               reinterpret_cast<int*>(small + 12));
     GT_LAUNCH(gtd::deg64_kernel, ceil_div(n, 256), 256, 0, o.deg, n, und_off);

@@ -22,6 +22,16 @@ def golden_cases() -> dict:
 
 
 @lru_cache(maxsize=1)
+def golden_traverse() -> dict:
+    """{case: {field: array}} of sssp / connected_components / k_core recorded
+    from the real reference (tests/golden/make_golden_traverse.py)."""
+    data = np.load(GOLDEN / "traverse.npz")
+    out = {}
+    for name in data["__names__"].tolist():
+        out[name] = {k.split("/", 1)[1]: data[k] for k in data.files if k.startswith(name + "/")}
+    return out
+
+
 def golden_c1() -> dict:
     data = np.load(GOLDEN / "c1.npz")
     return {k: data[k] for k in data.files}

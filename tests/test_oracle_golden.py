@@ -66,3 +66,37 @@ def test_parallel_sort_equals_np_sort():
     v = rng.integers(0, 1 << 40, size=300_000).astype(np.uint64)
     for w in (1, 3, 8):
         assert np.array_equal(ref.parallel_sort(v, w), np.sort(v))
+
+
+# ---- sssp / connected_components / k_core --------------
+
+TRAVERSE = sorted(__import__("helpers").golden_traverse())
+
+
+def _traverse_csr(case):
+    g = ref.build_csr(case["src"], case["dst"], workers=1)
+    return ref.add_isolated(g, case["extra"]) if case["extra"].size else g
+
+
+@pytest.mark.parametrize("name", TRAVERSE)
+def test_oracle_traversals_match_reference(name):
+    from helpers import golden_traverse
+
+    case = golden_traverse()[name]
+    g = _traverse_csr(case)
+    assert np.array_equal(g.ids, case["ids"])
+    und = ref.undirected_dense(g)
+    for row, s in zip(case["sssp"], case["sources"].tolist()):
+        assert np.array_equal(ref.sssp_csr(g, int(np.searchsorted(g.ids, s))), row)
+    assert np.array_equal(ref.components_csr(g, und), case["cc"])
+    for k in (1, 2, 3, 4):
+        core = ref.k_core_csr(g, k, und)
+        assert np.array_equal(core.ids, case[f"kcore{k}_ids"])
+        assert np.array_equal(core.out_off, case[f"kcore{k}_out_off"])
+        assert np.array_equal(core.out_adj, case[f"kcore{k}_out_adj"])
+
+
+def test_oracle_k_core_rejects_k0():
+    g = ref.build_csr([0], [1])
+    with pytest.raises(ValueError):
+        ref.k_core_csr(g, 0)
