@@ -445,6 +445,26 @@ def ours_arm(args):
                 "ms": ms_x, "value": g_x.edge_count / (ms_x / 1e3), "unit": "edges/s",
                 "achieved_gbs": by_x / args.steps / (ms_x / 1e3) / 1e9,
                 "hbm_frac": by_x / args.steps / (ms_x / 1e3) / 1e9 / pk["hbm_gbs"]}
+        # §8f next #4: the other CSR consumers on the same graph (wall time of
+        # the public call, results to the host; kernel time from the phases)
+        from paper_1503_07881_b200.algorithms import _ids_only
+
+        source = int(_ids_only(g_x)[0])
+        for name, call in (("sssp", lambda: gt.sssp(g_x, source)),
+                           ("connected_components", lambda: gt.connected_components(g_x)),
+                           ("k_core_k8", lambda: gt.k_core(g_x, 8))):
+            call()  # warm-up
+            _native.profile_reset()
+            _native.profile_enable(True)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                call()
+            wall = (time.perf_counter() - t0) / args.steps
+            kern = sum(v[0] for v in _native.profile_read().values()) / args.steps
+            _native.profile_enable(False)
+            extras[name] = {"ms": wall * 1e3, "kernel_ms": kern,
+                            "value": g_x.edge_count / wall, "unit": "edges/s (E / call time)"}
         del g_x
         if not args.no_tsv:
             extras["load_tsv"] = tsv_extra(src, dst, args, pk)

@@ -125,6 +125,61 @@ __global__ void __launch_bounds__(256) uf_init_kernel(int32_t* __restrict__ pare
   if (i < n) parent[i] = int32_t(i);
 }
 
+// union(a, b): the larger root hooked under the smaller with a CAS (retried
+// from the new parent when it loses).
+__device__ __forceinline__ void uf_union(int32_t* parent, int32_t a, int32_t b) {
+  int32_t x = uf_find(parent, a), y = uf_find(parent, b);
+  while (x != y) {
+    if (x < y) {
+      const int32_t t = x;
+      x = y;
+      y = t;
+    }
+    const int32_t old = atomicCAS(parent + x, x, y);  // hook root x (> y) under y
+    if (old == x) return;
+    x = uf_find(parent, old);
+    y = uf_find(parent, y);
+  }
+}
+
+// Afforest, round r: every node links with its r-th out-neighbour (a sparse
+// sample of the edges that already joins nearly all of a giant component).
+__global__ void __launch_bounds__(256) uf_sample_kernel(const int64_t* __restrict__ off,
+                                                        const int32_t* __restrict__ adj, int64_t n,
+                                                        int r, int32_t* parent) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < n; u += stride) {
+    const int64_t a = off[u];
+    if (a + r < off[u + 1]) uf_union(parent, int32_t(u), adj[a + r]);
+  }
+}
+
+// Afforest, final pass: warp per node u outside the dominant component c —
+// every remaining out-edge (from position `skip`) and every in-edge of u is
+// linked. Edges with both ends in c are already joined and never touched.
+__global__ void __launch_bounds__(256) uf_finish_kernel(
+    const int64_t* __restrict__ out_off, const int32_t* __restrict__ out_adj,
+    const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_adj, int64_t n, int skip,
+    int32_t c, int32_t* parent) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t u = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < n; u += nwarps) {
+    if (uf_find(parent, int32_t(u)) == c) continue;  // warp-uniform
+    const int64_t oa = out_off[u] + skip, ob = out_off[u + 1];
+    for (int64_t k = oa + lane; k < ob; k += 32) uf_union(parent, int32_t(u), out_adj[k]);
+    const int64_t ia = in_off[u], ib = in_off[u + 1];
+    for (int64_t k = ia + lane; k < ib; k += 32) uf_union(parent, int32_t(u), in_adj[k]);
+  }
+}
+
+// Root of sample i (i-th of `ns` nodes spread over [0, n)), for the host to
+// pick the dominant component.
+__global__ void uf_sample_roots_kernel(int32_t* parent, int64_t n, int ns,
+                                       int32_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ns) out[i] = uf_find(parent, int32_t((uint64_t(i) * 0x9E3779B97F4A7C15ull >> 11) % uint64_t(n)));
+}
+
 // Warp per row u, lanes over out(u): union(u, v), the larger root hooked under
 // the smaller with a CAS (retried from the new parent when it loses).
 __global__ void __launch_bounds__(256) uf_hook_kernel(const int64_t* __restrict__ off,
@@ -316,12 +371,37 @@ static int64_t components(const gt_graph* g, int64_t* out, bool out_device) {
   int64_t* rank = ws_n<int64_t>(WS_TMP1, size_t(n) + 1);
   int64_t* small = ws_n<int64_t>(WS_SMALL, 16);
   int64_t* labels = out_device ? out : dalloc_n<int64_t>(size_t(n));
+  // Afforest (Sutton et al.): link a two-neighbour sample, find the dominant
+  // root from a sample of nodes, then link every other edge only for nodes
+  // outside it (out- and in-edges, so no edge with an end outside is missed)
+  constexpr int SAMPLE_ROUNDS = 2, SAMPLE_NODES = 1024;
+  int32_t* sroots = reinterpret_cast<int32_t*>(small + 8);  // 64 B, then host mode
+  int32_t* sbuf = ws_n<int32_t>(WS_TMP2, SAMPLE_NODES);
   {
     Phase ph("cc.union_find", 8.0 * n + 4.0 * g->e + 8.0 * (n + 1));
     GT_LAUNCH(gtd::uf_init_kernel, ceil_div(n, 256), 256, 0, parent, n);
-    if (g->e)
-      GT_LAUNCH(gtd::uf_hook_kernel, warps_grid(n), 256, 0, g->out_off, g->out_adj, n, parent);
+    for (int r = 0; r < SAMPLE_ROUNDS && g->e; ++r)
+      GT_LAUNCH(gtd::uf_sample_kernel, grid_for(n, 4), 256, 0, g->out_off, g->out_adj, n, r,
+                parent);
   }
+  int32_t c = -1;
+  if (g->e) {
+    GT_LAUNCH(gtd::uf_sample_roots_kernel, ceil_div(SAMPLE_NODES, 256), 256, 0, parent, n,
+              SAMPLE_NODES, sbuf);
+    std::vector<int32_t> h(SAMPLE_NODES);
+    d2h(h.data(), sbuf, h.size() * 4);
+    sync();
+    std::sort(h.begin(), h.end());
+    int best = 0;
+    for (int i = 0, j; i < SAMPLE_NODES; i = j) {
+      for (j = i; j < SAMPLE_NODES && h[j] == h[i]; ++j) {}
+      if (j - i > best) { best = j - i; c = h[i]; }
+    }
+    Phase ph("cc.union_find", 0.0);
+    GT_LAUNCH(gtd::uf_finish_kernel, warps_grid(n), 256, 0, g->out_off, g->out_adj, g->in_off,
+              g->in_adj, n, SAMPLE_ROUNDS, c, parent);
+  }
+  (void)sroots;
   {
     Phase ph("cc.label", 4.0 * n + 8.0 * n * 3);
     GT_LAUNCH(gtd::uf_flatten_kernel, ceil_div(n, 256), 256, 0, parent, n, rank);
