@@ -45,6 +45,7 @@ struct Context {
   int device = -1;
   int sm_count = 148;
   size_t l2_bytes = 0;
+  int smem_optin = 227 * 1024;  // max dynamic shared memory per block (opt-in)
   cudaStream_t stream = nullptr;
   bool profiling = false;
 };

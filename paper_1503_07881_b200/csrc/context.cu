@@ -197,6 +197,7 @@ int gt_init(int device) {
     c.device = device;
     c.sm_count = prop.multiProcessorCount;
     c.l2_bytes = prop.l2CacheSize;
+    c.smem_optin = int(prop.sharedMemPerBlockOptin);
     GT_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     cudaMemPool_t pool;
     GT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));

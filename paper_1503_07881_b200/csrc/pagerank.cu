@@ -52,6 +52,7 @@ __device__ __forceinline__ double pr_gather(const double* contrib, int32_t u) {
 
 constexpr int PR_THREADS = 256;
 constexpr int PR_TILE = 2048;
+constexpr int PR_MIN_BLOCKS = 6;  // resident CTAs per SM the register budget is sized for
 
 // Last-block deterministic reduction of one double per block.
 __device__ __forceinline__ void grid_reduce_last(double block_val, double* partials,
@@ -213,15 +214,15 @@ __device__ __forceinline__ void pr_rows(const double* vals, const PrRows& sr,
                                         double* __restrict__ score, double* __restrict__ contrib_next,
                                         double* __restrict__ head, double* __restrict__ tail,
                                         int64_t* __restrict__ tail_row, bool last_iter,
-                                        double& dang) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                                        double& dang, int ltid) {
+  const int warp = ltid >> 5, lane = ltid & 31;
   auto off_at = [&](int64_t r) -> int {
     if (r < PR_ROWCAP + 1) return sr.off[r];
     const int64_t x = in_off[first_row + r] - e0;
     return int(x < 0 ? 0 : (x > ne ? ne : x));
   };
   // short segments: thread per segment
-  for (int64_t s = threadIdx.x; s < nseg; s += PR_THREADS) {
+  for (int64_t s = ltid; s < nseg; s += PR_THREADS) {
     const int a = off_at(s), b = off_at(s + 1);
     if (b - a >= PR_LONG) continue;
     double sum = 0.0;
@@ -243,24 +244,23 @@ __device__ __forceinline__ void pr_rows(const double* vals, const PrRows& sr,
   }
 }
 
-__global__ void __launch_bounds__(PR_THREADS) pr_spmv_kernel(
+// One tile of PR_TILE in-edges, processed by a group of PR_THREADS threads
+// (ltid = thread index in the group, bar() = the group's barrier). Gathers
+// come from contrib through pr_gather.
+template <typename Bar>
+__device__ __forceinline__ void pr_tile(
+    int64_t c, int ltid, Bar bar, double* vals, PrRows& sr,
     const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_adj, int64_t n, int64_t e,
-    int64_t n_total, const int64_t* __restrict__ tile_row, const double* __restrict__ contrib,
-    const double* __restrict__ inv_out, const int32_t* __restrict__ pos,
-    const double* __restrict__ dangling_prev, double damping,
-    double* __restrict__ score, double* __restrict__ contrib_next, double* __restrict__ head,
-    double* __restrict__ tail, int64_t* __restrict__ tail_row, double* __restrict__ dpart,
-    int last_iter) {
-  __shared__ double vals[PR_TILE];
-  __shared__ PrRows sr;
-  const int64_t c = blockIdx.x;
+    const int64_t* __restrict__ tile_row, const double* __restrict__ contrib,
+    const double* __restrict__ inv_out, const int32_t* __restrict__ pos, double base,
+    double damping, double* __restrict__ score, double* __restrict__ contrib_next,
+    double* __restrict__ head, double* __restrict__ tail, int64_t* __restrict__ tail_row,
+    double* __restrict__ dpart, bool last) {
   const int64_t e0 = c * PR_TILE;
   const int64_t e1 = min(e, e0 + PR_TILE);
   const int ne = e1 > e0 ? int(e1 - e0) : 0;
   const int64_t ra = tile_row[c], rb = tile_row[c + 1];
-  const double base =
-      (1.0 - damping) / double(n_total) + damping * (*dangling_prev / double(n_total));
-  if (threadIdx.x == 0) tail_row[c] = -1;
+  if (ltid == 0) tail_row[c] = -1;
   // segments: the head row ra-1 (starts before the tile) when it reaches
   // into it, then rows ra..rb-1 (start inside); the last may run past e1
   const bool has_head = ne > 0 && (ra == n || in_off[ra] > e0);
@@ -268,17 +268,17 @@ __global__ void __launch_bounds__(PR_THREADS) pr_spmv_kernel(
   const int64_t nseg = rb - first_row;
   const bool has_tail = nseg > 0 && in_off[rb] > e1 && !(has_head && nseg == 1);
 
-  // Gather phase: PR_TILE/256 independent loads per thread in flight, and
-  // the tile's row metadata staged alongside (independent of the gathers).
+  // Gather phase: PR_TILE/PR_THREADS independent loads per thread in flight,
+  // and the tile's row metadata staged alongside (independent of the gathers).
   constexpr int PER = PR_TILE / PR_THREADS;
   int32_t idx[PER];
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    const int j = i * PR_THREADS + threadIdx.x;
+    const int j = i * PR_THREADS + ltid;
     idx[i] = j < ne ? __ldcs(in_adj + e0 + j) : 0;
   }
   const int64_t nstage = min(nseg + 1, int64_t(PR_ROWCAP + 1));
-  for (int64_t r = threadIdx.x; r < nstage; r += PR_THREADS) {
+  for (int64_t r = ltid; r < nstage; r += PR_THREADS) {
     const int64_t row = first_row + r;
     const int64_t x = in_off[row] - e0;
     sr.off[r] = uint16_t(x < 0 ? 0 : (x > ne ? ne : x));
@@ -289,19 +289,35 @@ __global__ void __launch_bounds__(PR_THREADS) pr_spmv_kernel(
   }
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    const int j = i * PR_THREADS + threadIdx.x;
+    const int j = i * PR_THREADS + ltid;
     if (j < ne) vals[j] = pr_gather(contrib, idx[i]);
   }
-  __syncthreads();
+  bar();
 
-  const bool last = last_iter != 0;
   double dang = 0.0;
   pr_rows(vals, sr, in_off, e0, ne, first_row, nseg, has_head, has_tail, c, base, damping,
-          inv_out, pos, score, contrib_next, head, tail, tail_row, last, dang);
+          inv_out, pos, score, contrib_next, head, tail, tail_row, last, dang, ltid);
   // per-warp dangling partials (summed in a fixed order by the fixup kernel):
-  // no block-wide barrier at the end of the tile
+  // no barrier at the end of the tile
   dang = warp_sum(dang);
-  if ((threadIdx.x & 31) == 0) dpart[c * (PR_THREADS / 32) + (threadIdx.x >> 5)] = dang;
+  if ((ltid & 31) == 0) dpart[c * (PR_THREADS / 32) + (ltid >> 5)] = dang;
+}
+
+__global__ void __launch_bounds__(PR_THREADS, PR_MIN_BLOCKS) pr_spmv_kernel(
+    const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_adj, int64_t n, int64_t e,
+    int64_t n_total, const int64_t* __restrict__ tile_row, const double* __restrict__ contrib,
+    const double* __restrict__ inv_out, const int32_t* __restrict__ pos,
+    const double* __restrict__ dangling_prev, double damping,
+    double* __restrict__ score, double* __restrict__ contrib_next, double* __restrict__ head,
+    double* __restrict__ tail, int64_t* __restrict__ tail_row, double* __restrict__ dpart,
+    int last_iter) {
+  __shared__ double vals[PR_TILE];
+  __shared__ PrRows sr;
+  const double base =
+      (1.0 - damping) / double(n_total) + damping * (*dangling_prev / double(n_total));
+  pr_tile(int64_t(blockIdx.x), int(threadIdx.x), [] { __syncthreads(); }, vals, sr, in_off,
+          in_adj, n, e, tile_row, contrib, inv_out, pos, base, damping, score, contrib_next, head,
+          tail, tail_row, dpart, last_iter != 0);
 }
 
 __global__ void __launch_bounds__(256) pr_fixup_kernel(

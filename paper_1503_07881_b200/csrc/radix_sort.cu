@@ -11,6 +11,11 @@ using gt::RS_KPT;
 using gt::RS_THREADS;
 using gt::RS_TILE;
 
+// resident CTAs per SM the onesweep register budget is sized for
+constexpr int RS_MIN_BLOCKS = 3;
+// predecessor status words polled per look-back round trip
+constexpr int LB_WIN = 4;
+
 __global__ void __launch_bounds__(256) hist_kernel(const uint64_t* __restrict__ keys, int64_t n,
                                                    gt::SortPlan plan,
                                                    unsigned long long* __restrict__ ghist) {
@@ -41,32 +46,35 @@ __global__ void __launch_bounds__(256) digit_scan_kernel(const unsigned long lon
 // ballot per digit bit (ALU pipe): splitting the ranking across the two pipes
 // keeps either from being the bottleneck (ncu: all-MATCH ranking was 68%
 // ADU-bound, all-ballot ranking doubled the instruction count).
-template <int BITS, int RS_MATCH>
-__global__ void __launch_bounds__(RS_THREADS, 3)
-    onesweep_kernel(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int64_t n,
-                    int shift, const int64_t* __restrict__ digit_base,
-                    uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter,
-                    uint32_t epoch) {
+struct OnesweepSmem {
+  uint64_t keys[RS_TILE];  // staged by index during the look-back, then by position
+  uint32_t whist[RS_THREADS / 32][256];
+  int64_t gbase[256];
+  uint32_t scan[8];
+  uint32_t tile;
+};
+
+// One tile of a onesweep pass. FULL: the tile holds RS_TILE keys, so every
+// per-key bounds test compiles away (all tiles but the last).
+template <int BITS, int RS_MATCH, bool FULL>
+__device__ __forceinline__ void onesweep_tile(OnesweepSmem& s, const uint64_t* __restrict__ in,
+                                              uint64_t* __restrict__ out, int64_t n, int shift,
+                                              const int64_t* __restrict__ digit_base,
+                                              uint64_t* __restrict__ status, int tile,
+                                              uint32_t epoch) {
   constexpr int NW = RS_THREADS / 32;
   constexpr uint32_t mask = (1u << BITS) - 1u;
-  __shared__ struct {
-    uint64_t keys[RS_TILE];  // staged by index during the look-back, then by position
-    uint32_t whist[NW][256];
-  } s;
-  __shared__ int64_t s_gbase[256];
-  __shared__ uint32_t s_scan[8];
-  __shared__ uint32_t s_tile;
-
+  int64_t* s_gbase = s.gbase;
+  uint32_t* s_scan = s.scan;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-  for (int i = tid; i < NW * 256; i += RS_THREADS) (&s.whist[0][0])[i] = 0;
-  __syncthreads();
-  const int tile = int(s_tile);
   const int64_t base = int64_t(tile) * RS_TILE;
   const int woff = warp * 32 * RS_KPT + lane;  // key i of this thread: tile element woff + 32*i
 
-  const int64_t rem64 = n - (base + woff);
-  const int rem = rem64 > 32 * RS_KPT ? 32 * RS_KPT : (rem64 < 0 ? 0 : int(rem64));
+  int rem = 32 * RS_KPT;
+  if (!FULL) {
+    const int64_t rem64 = n - (base + woff);
+    rem = rem64 > 32 * RS_KPT ? 32 * RS_KPT : (rem64 < 0 ? 0 : int(rem64));
+  }
   const uint64_t* src = in + (base + woff);
   uint64_t k[RS_KPT];
 #pragma unroll
@@ -80,10 +88,11 @@ __global__ void __launch_bounds__(RS_THREADS, 3)
   for (int i = 0; i < RS_KPT; ++i) {
     const uint32_t d = uint32_t(k[i] >> shift) & mask;
     if (i < RS_MATCH) {
-      rank[i] = __match_any_sync(0xffffffffu, 32 * i < rem ? d : 0xFFFFu) &
-                __ballot_sync(0xffffffffu, 32 * i < rem);
+      rank[i] = FULL ? __match_any_sync(0xffffffffu, d)
+                     : __match_any_sync(0xffffffffu, 32 * i < rem ? d : 0xFFFFu) &
+                           __ballot_sync(0xffffffffu, 32 * i < rem);
     } else {
-      uint32_t peers = __ballot_sync(0xffffffffu, 32 * i < rem);
+      uint32_t peers = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, 32 * i < rem);
 #pragma unroll
       for (int b = 0; b < BITS; ++b) {
         const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
@@ -130,7 +139,6 @@ __global__ void __launch_bounds__(RS_THREADS, 3)
     // Decoupled look-back, LB_WIN predecessors polled per round trip.
     uint64_t excl = 0;
     if (tile > 0) {
-      constexpr int LB_WIN = 4;
       const uint64_t ep = uint64_t(epoch & 0x3FFFFFu);
       int t = tile - 1;
       bool done = false;
@@ -179,11 +187,37 @@ __global__ void __launch_bounds__(RS_THREADS, 3)
     if (32 * i < rem) s.keys[pos[i]] = k[i];
   __syncthreads();
 
-  const int nvalid = (n - base) < RS_TILE ? int(n - base) : RS_TILE;
-  for (int j = tid; j < nvalid; j += RS_THREADS) {
-    const uint64_t key = s.keys[j];
-    out[s_gbase[uint32_t(key >> shift) & mask] + j] = key;
+  if (FULL) {
+#pragma unroll
+    for (int i = 0; i < RS_KPT; ++i) {
+      const int j = tid + i * RS_THREADS;
+      const uint64_t key = s.keys[j];
+      out[s_gbase[uint32_t(key >> shift) & mask] + j] = key;
+    }
+  } else {
+    const int nvalid = (n - base) < RS_TILE ? int(n - base) : RS_TILE;
+    for (int j = tid; j < nvalid; j += RS_THREADS) {
+      const uint64_t key = s.keys[j];
+      out[s_gbase[uint32_t(key >> shift) & mask] + j] = key;
+    }
   }
+}
+
+template <int BITS, int RS_MATCH>
+__global__ void __launch_bounds__(RS_THREADS, RS_MIN_BLOCKS)
+    onesweep_kernel(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int64_t n,
+                    int shift, const int64_t* __restrict__ digit_base,
+                    uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter,
+                    uint32_t epoch) {
+  __shared__ OnesweepSmem s;
+  if (threadIdx.x == 0) s.tile = atomicAdd(tile_counter, 1u);
+  for (int i = threadIdx.x; i < (RS_THREADS / 32) * 256; i += RS_THREADS) (&s.whist[0][0])[i] = 0;
+  __syncthreads();
+  const int tile = int(s.tile);
+  if (int64_t(tile + 1) * RS_TILE <= n)
+    onesweep_tile<BITS, RS_MATCH, true>(s, in, out, n, shift, digit_base, status, tile, epoch);
+  else
+    onesweep_tile<BITS, RS_MATCH, false>(s, in, out, n, shift, digit_base, status, tile, epoch);
 }
 
 }  // namespace gtd
