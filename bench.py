@@ -153,6 +153,67 @@ def reference_arm(args):
 
 # ----------------------------------------------------------------------- ours
 
+def relational_extras(table, rows, args, pk):
+    """device Select and Join on the bench's edge table
+    (select src < median id: ~half the rows; join the edge table (probe) with
+    a node-attribute table of up to 1M distinct src ids (build) on src). Wall time of the public
+    call (device-resident result) and kernel time from the library phases."""
+    import torch
+
+    import paper_1503_07881_b200 as gt
+    from paper_1503_07881_b200 import _native
+
+    out = {}
+    src = table.column("src")
+    thr = int(torch.median(src[: 1 << 20]).item())
+    n_attr = 1 << 20
+    nodes = torch.unique(src[:: max(1, rows // (4 * n_attr))])[:n_attr]  # distinct keys
+    attr = gt.ColumnTable(gt.Schema([("node", "int"), ("score", "int")]),
+                          [nodes, torch.arange(nodes.shape[0], dtype=torch.int64,
+                                               device=src.device)])
+    cases = (("select", lambda: gt.select(table, gt.Predicate("src", "<", thr))),
+             ("join", lambda: gt.join(attr, table, "node", "src")))
+    for name, call in cases:
+        res = call()  # warm-up
+        n_out = res.n_rows
+        del res
+        _native.profile_reset()
+        _native.profile_enable(True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            res = call()
+            del res
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) / args.steps
+        ph = _native.profile_read()
+        _native.profile_enable(False)
+        kern = sum(v[0] for v in ph.values()) / args.steps
+        kb = sum(v[2] for v in ph.values()) / args.steps
+        out[name] = {"ms": wall * 1e3, "kernel_ms": kern, "rows_in": rows, "rows_out": n_out,
+                     "value": rows / wall, "unit": "input rows/s (call time)",
+                     "kernel_gbs": kb / (kern / 1e3) / 1e9 if kern > 0 else None,
+                     "kernel_hbm_frac": (kb / (kern / 1e3) / 1e9 / pk["hbm_gbs"]
+                                         if kern > 0 else None)}
+    if not args.no_cpu_baseline:  # the oracle port (reference algorithm) on a 1M-row sample
+        from oracle import reference_port as ref_port
+
+        m = min(rows, 1_000_000)
+        h_src = src[:m].cpu().numpy()
+        h_nodes = attr.column("node").cpu().numpy()
+        t0 = time.perf_counter()
+        ref_port.select_indices(h_src, "int", [], "<", thr)
+        t_sel = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        ref_port.join_indices(h_nodes.tolist(), h_src.tolist())
+        t_join = time.perf_counter() - t0
+        for name, t in (("select", t_sel), ("join", t_join)):
+            out[name]["cpu_port"] = {"rows": m, "s": t, "value": m / t,
+                                     "unit": "input rows/s", "cores": 1,
+                                     "kind": "port (oracle/reference_port.py)"}
+    return out
+
+
 def tsv_extra(src, dst, args, pk):
     """§8f next #2: LoadTableTSV of an int64 edge TSV on the GPU (file read +
     H2D + parse, wall clock) and the parse kernels alone, on the first
@@ -466,6 +527,7 @@ def ours_arm(args):
             extras[name] = {"ms": wall * 1e3, "kernel_ms": kern,
                             "value": g_x.edge_count / wall, "unit": "edges/s (E / call time)"}
         del g_x
+        extras.update(relational_extras(table, rows, args, pk))
         if not args.no_tsv:
             extras["load_tsv"] = tsv_extra(src, dst, args, pk)
 

@@ -54,6 +54,7 @@ extern "C" {
 #endif
 
 typedef struct gt_graph gt_graph;
+typedef struct gt_join gt_join;
 
 /* ---- context ------------------------------------------------------------ */
 
@@ -181,6 +182,45 @@ GT_API int gt_connected_components(const gt_graph* g, int64_t* labels, int label
  * node set whose members keep >= k distinct undirected neighbours inside it,
  * as a new graph (free with gt_graph_free). GT_EINVAL for k < 1. */
 GT_API int gt_kcore(const gt_graph* g, int k, gt_graph** out);
+
+/* ---- relational operators feeding ToGraph -------- */
+
+/* Predicate comparison codes (tables.py:32-39 _COMPARATORS). */
+#define GT_CMP_EQ 0
+#define GT_CMP_NE 1
+#define GT_CMP_LT 2
+#define GT_CMP_LE 3
+#define GT_CMP_GT 4
+#define GT_CMP_GE 5
+
+/* Select (tables.py:325-344): ascending indices of the rows of the device
+ * column d_col[n] whose value satisfies `value op constant`.
+ *   kind 0: int64 column vs ival (INT; STRING = / != on pool codes)
+ *   kind 1: float64 column vs fval (IEEE, as numpy: NaN only satisfies !=)
+ *   kind 2: int64 codes, row selected iff 0 <= code < lut_n and d_lut[code]
+ *           (STRING ordering comparisons, evaluated on the decoded pool)
+ * d_out_idx holds n entries; *n_out (host) = number of rows selected. */
+GT_API int gt_select_rows(const void* d_col, int64_t n, int kind, int op, int64_t ival,
+                          double fval, const uint8_t* d_lut, int64_t lut_n, int64_t* d_out_idx,
+                          int64_t* n_out);
+
+/* Row gather of one 8-byte column (ColumnTable._take tables.py:232-240,
+ * _paired_table tables.py:385-394): d_out[i] = d_src[d_idx[i]] (d_idx NULL:
+ * identity), then, if d_remap is not NULL, d_out[i] = d_remap[d_out[i]]
+ * (right-pool string codes into the merged pool, tables.py:393). */
+GT_API int gt_gather_u64(const uint64_t* d_src, const int64_t* d_idx, int64_t n,
+                         const int64_t* d_remap, uint64_t* d_out);
+
+/* Equi-join (tables.py:397-426) of device key columns d_left[nl], d_right[nr]
+ * (kind 0: int64 keys; kind 1: float64 keys with -0.0 == 0.0 and NaN never
+ * matching). Builds on the smaller side (left when nl <= nr); the pairs come
+ * out in the reference's order: probe row ascending, then build row ascending.
+ * *out owns the (left row, right row) pair lists; *n_pairs = their length. */
+GT_API int gt_join_build(const void* d_left, int64_t nl, const void* d_right, int64_t nr,
+                         int kind, gt_join** out, int64_t* n_pairs);
+/* Copy the pair lists into device buffers of n_pairs int64 each. */
+GT_API int gt_join_export(const gt_join* j, int64_t* d_left_rows, int64_t* d_right_rows);
+GT_API void gt_join_free(gt_join* j);
 
 /* ---- synthetic inputs (bench / tests; no reference counterpart) --------- */
 

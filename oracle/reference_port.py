@@ -390,3 +390,55 @@ def add_isolated(g: CSR, extra) -> CSR:
     out_off = np.concatenate(([0], np.cumsum(out_deg))).astype(np.int64)
     in_off = np.concatenate(([0], np.cumsum(in_deg))).astype(np.int64)
     return CSR(ids, out_off, g.out_adj, in_off, g.in_adj)
+
+
+# ------------------------------------------------------ tables.py: select / join
+
+_CMP = {"=": np.equal, "!=": np.not_equal, "<": np.less, "<=": np.less_equal,
+        ">": np.greater, ">=": np.greater_equal}
+
+
+def select_indices(col, typ, pool, op, value):
+    """tables.py:325-344 — ascending indices of the rows that satisfy the
+    predicate. col: int64 (int / str codes) or float64 numpy column."""
+    col = np.asarray(col)
+    if typ == "str":
+        if op in ("=", "!="):
+            # encode_value (tables.py:201-205): pool code or None
+            code = {s: i for i, s in enumerate(pool)}.get(value)
+            if code is None:
+                mask = np.full(col.shape[0], op == "!=", dtype=bool)
+            else:
+                mask = _CMP[op](col, code)
+        else:  # ordering comparisons on the decoded strings (tables.py:339-341)
+            import operator
+            cmp = {"<": operator.lt, "<=": operator.le, ">": operator.gt,
+                   ">=": operator.ge}[op]
+            mask = np.array([cmp(pool[c], value) for c in col.tolist()], dtype=bool)
+    else:
+        mask = _CMP[op](col, value)
+    return np.flatnonzero(mask).astype(np.int64)
+
+
+def join_indices(lkeys, rkeys):
+    """tables.py:397-426 — (left rows, right rows) of the equi-join: hash join
+    building on the smaller side (left when len(left) <= len(right)), pairs in
+    probe-row order and, per probe row, build rows in ascending order. Keys are
+    python-comparable values (decoded strings, ints or floats), so dict
+    semantics apply (-0.0 == 0.0, NaN never equal to another NaN object)."""
+    lkeys = list(lkeys)
+    rkeys = list(rkeys)
+    build_left = len(lkeys) <= len(rkeys)
+    bkeys, pkeys = (lkeys, rkeys) if build_left else (rkeys, lkeys)
+    buckets = {}
+    for i, k in enumerate(bkeys):
+        buckets.setdefault(k, []).append(i)
+    bi, pi = [], []
+    for i, k in enumerate(pkeys):
+        hit = buckets.get(k)
+        if hit:
+            bi.extend(hit)
+            pi.extend([i] * len(hit))
+    bi = np.asarray(bi, dtype=np.int64)
+    pi = np.asarray(pi, dtype=np.int64)
+    return (bi, pi) if build_left else (pi, bi)

@@ -24,6 +24,7 @@ from .errors import (
     UnknownNodeError,
 )
 from .graph import DeviceGraph, Graph, NodeRecord, from_edges, upload
+from .relational import Predicate, join, project, select
 from .tables import (FLOAT, INT, STRING, ColumnTable, Schema, edge_table, load_tsv, save_tsv,
                      table_from_map)
 
@@ -36,5 +37,5 @@ __all__ = [
     "edge_table", "from_edges", "graph_to_edge_table", "graph_to_node_table", "load_tsv",
     "pagerank", "pagerank_device", "save_tsv", "table_from_map", "table_to_graph",
     "triangle_count", "upload", "sssp", "connected_components", "k_core", "DistMap",
-    "LabelMap",
+    "LabelMap", "Predicate", "select", "project", "join",
 ]

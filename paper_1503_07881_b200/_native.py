@@ -81,6 +81,14 @@ SIGNATURES = {
                                         _VP, _VP, _VP, ctypes.c_double, ctypes.c_int, _VP, _VP,
                                         _VP]),
     "gt_triangles_part": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, _I64P]),
+    "gt_select_rows": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_int64, ctypes.c_double, _VP, ctypes.c_int64, _VP,
+                                      _I64P]),
+    "gt_gather_u64": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, _VP, _VP]),
+    "gt_join_build": (ctypes.c_int, [_VP, ctypes.c_int64, _VP, ctypes.c_int64, ctypes.c_int,
+                                     ctypes.POINTER(_VP), _I64P]),
+    "gt_join_export": (ctypes.c_int, [_VP, _VP, _VP]),
+    "gt_join_free": (None, [_VP]),
     "gt_launch_count": (ctypes.c_int64, []),
     "gt_profile_enable": (ctypes.c_int, [ctypes.c_int]),
     "gt_profile_reset": (ctypes.c_int, []),
@@ -286,6 +294,42 @@ def triangle_orientation(handle: int, n: int):
     check(lib.gt_triangle_orientation(handle, None, None, None, _ptr(adj_p), ctypes.byref(m)),
           "gt_triangle_orientation")
     return deg, rank, off_p, adj_p
+
+
+def select_rows(col_ptr: int, n: int, kind: int, op: int, ival: int, fval: float,
+                lut_ptr: int | None, lut_n: int, out_ptr: int) -> int:
+    """Device select -> number of selected rows (indices written to out_ptr)."""
+    lib = ensure_init()
+    m = ctypes.c_int64()
+    check(lib.gt_select_rows(col_ptr or None, int(n), int(kind), int(op), int(ival), float(fval),
+                             lut_ptr or None, int(lut_n), out_ptr or None, ctypes.byref(m)),
+          "gt_select_rows")
+    return int(m.value)
+
+
+def gather_u64(src_ptr: int, idx_ptr: int | None, n: int, remap_ptr: int | None,
+               out_ptr: int) -> None:
+    lib = ensure_init()
+    check(lib.gt_gather_u64(src_ptr or None, idx_ptr or None, int(n), remap_ptr or None,
+                            out_ptr or None), "gt_gather_u64")
+
+
+def join_pairs(left_ptr: int, nl: int, right_ptr: int, nr: int, kind: int, alloc):
+    """Device equi-join -> (left rows, right rows) as two int64 device buffers
+    obtained from ``alloc(n)``."""
+    lib = ensure_init()
+    h = _VP()
+    m = ctypes.c_int64()
+    check(lib.gt_join_build(left_ptr or None, int(nl), right_ptr or None, int(nr), int(kind),
+                            ctypes.byref(h), ctypes.byref(m)), "gt_join_build")
+    try:
+        n = int(m.value)
+        li, ri = alloc(n), alloc(n)
+        check(lib.gt_join_export(h, li.data_ptr() if n else None, ri.data_ptr() if n else None),
+              "gt_join_export")
+        return li, ri
+    finally:
+        lib.gt_join_free(h)
 
 
 def graph_edge_table(handle: int, src, dst, on_device: bool):

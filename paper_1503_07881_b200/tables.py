@@ -78,9 +78,11 @@ def _length(col) -> int:
 
 
 class ColumnTable:
-    """Schema-typed columns of equal length (host numpy or device tensors)."""
+    """Schema-typed columns of equal length (host numpy or device tensors);
+    every row carries a persistent id (tables.py:136-150): fresh tables
+    number their rows 0..n-1, ``select`` keeps the ids of the surviving rows."""
 
-    def __init__(self, schema: Schema, columns, pool=None):
+    def __init__(self, schema: Schema, columns, pool=None, row_ids=None, next_row_id=None):
         if len(columns) != len(schema):
             raise SchemaError("column count does not match schema")
         cols = [c if _is_device(c) else np.asarray(c) for c in columns]
@@ -90,6 +92,71 @@ class ColumnTable:
         self.schema = schema
         self.columns = cols
         self.pool = pool if pool is not None else []
+        self._pool_index = None
+        n = _length(cols[0]) if cols else 0
+        if row_ids is not None and _length(row_ids) != n:
+            raise SchemaError("row_ids length does not match the columns")
+        self._row_ids = row_ids
+        if next_row_id is None:
+            next_row_id = n if row_ids is None else (int(row_ids.max()) + 1 if n else 0)
+        self._next_row_id = int(next_row_id)
+
+    @classmethod
+    def from_rows(cls, schema: Schema, rows) -> "ColumnTable":
+        """Table from python row tuples, strings given decoded and pooled by
+        first occurrence (tables.py:158-178)."""
+        pool: list[str] = []
+        index: dict[str, int] = {}
+        cols = []
+        for j, (_, typ) in enumerate(schema.columns):
+            vals = [r[j] for r in rows]
+            if typ == STRING:
+                codes = np.empty(len(vals), dtype=np.int64)
+                for i, v in enumerate(vals):
+                    code = index.get(v)
+                    if code is None:
+                        code = index[v] = len(pool)
+                        pool.append(v)
+                    codes[i] = code
+                cols.append(codes)
+            else:
+                cols.append(np.asarray(vals, dtype=np.float64 if typ == FLOAT else np.int64))
+        return cls(schema, cols, pool=pool)
+
+    @property
+    def row_ids(self):
+        """Persistent row ids (int64, same residency as the first column)."""
+        if self._row_ids is None:
+            n = self.n_rows
+            if self.columns and _is_device(self.columns[0]):
+                import torch
+
+                self._row_ids = torch.arange(n, dtype=torch.int64, device=self.columns[0].device)
+            else:
+                self._row_ids = np.arange(n, dtype=np.int64)
+        return self._row_ids
+
+    def decoded(self, name: str):
+        """Host column values with string codes decoded through the pool
+        (tables.py:193-199)."""
+        idx = self.schema.index_of(name)
+        col = self.columns[idx]
+        col = col.cpu().numpy() if _is_device(col) else col
+        if self.schema.columns[idx][1] == STRING:
+            return (np.asarray(self.pool, dtype=object)[col] if col.size
+                    else np.empty(0, dtype=object))
+        return col
+
+    def encode_value(self, value: str):
+        """Pool code of a string, or None when it is not pooled (tables.py:201-205)."""
+        if self._pool_index is None:
+            self._pool_index = {v: i for i, v in enumerate(self.pool)}
+        return self._pool_index.get(value)
+
+    def cell_equal(self, other: "ColumnTable") -> bool:
+        """Same schema and decoded cells row by row, row ids ignored (tables.py:219-223)."""
+        return (self.schema == other.schema and self.n_rows == other.n_rows
+                and self.to_rows() == other.to_rows())
 
     @property
     def n_rows(self) -> int:
@@ -101,20 +168,30 @@ class ColumnTable:
     def is_device_resident(self, name: str) -> bool:
         return _is_device(self.column(name))
 
-    def to_device(self, device="cuda") -> "ColumnTable":
-        """Copy of the table whose int columns live in HBM (torch int64)."""
+    def to_device(self, device="cuda", all_columns=False) -> "ColumnTable":
+        """Copy of the table whose int columns (every column with
+        ``all_columns``: str codes as int64, floats as float64) live in HBM."""
         import torch
 
         cols = []
         for (name, typ), col in zip(self.schema.columns, self.columns):
-            if typ == INT and not _is_device(col):
-                col = torch.from_numpy(np.ascontiguousarray(col, dtype=np.int64)).to(device)
+            if (typ == INT or all_columns) and not _is_device(col):
+                dt = np.float64 if typ == FLOAT else np.int64
+                col = torch.from_numpy(np.ascontiguousarray(col, dtype=dt)).to(device)
             cols.append(col)
-        return ColumnTable(self.schema, cols, pool=self.pool)
+        ids = self._row_ids
+        if ids is not None and all_columns and not _is_device(ids):
+            ids = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int64)).to(device)
+        return ColumnTable(self.schema, cols, pool=self.pool, row_ids=ids,
+                           next_row_id=self._next_row_id)
 
     def to_host(self) -> "ColumnTable":
         cols = [c.cpu().numpy() if _is_device(c) else c for c in self.columns]
-        return ColumnTable(self.schema, cols, pool=self.pool)
+        ids = self._row_ids
+        if ids is not None and _is_device(ids):
+            ids = ids.cpu().numpy()
+        return ColumnTable(self.schema, cols, pool=self.pool, row_ids=ids,
+                           next_row_id=self._next_row_id)
 
     def to_rows(self) -> list[tuple]:
         host = self.to_host()

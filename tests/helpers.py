@@ -76,3 +76,65 @@ def cubic_triangles(sym_adj):
     a = sym_adj.astype(np.float64)
     np.fill_diagonal(a, 0.0)
     return int(round(np.einsum("ij,jk,ki->", a, a, a) / 6.0))
+
+
+# ---------------------------------------------------------- select / join goldens
+
+REL_SCHEMA = (("k", "int"), ("x", "float"), ("s", "str"), ("v", "int"))
+
+
+def decode_const(text: str):
+    """Predicate constant written by make_golden_relational.encode_value."""
+    tag, val = text[:2], text[2:]
+    if tag == "s:":
+        return val
+    if tag == "f:":
+        return float.fromhex(val)
+    return int(val)
+
+
+@lru_cache(maxsize=1)
+def golden_relational() -> dict:
+    """Select / join outputs of the real reference (make_golden_relational.py):
+    {"tables": [(columns dict, pool list)], "preds": [(col, op, value)],
+     "sel": {(t, i): row ids}, "joins": [dict], "qa": dict}."""
+    d = np.load(GOLDEN / "relational.npz")
+    tabs = []
+    for t in range(int(d["n_tabs"][0])):
+        cols = {name: d[f"tab{t}_{name}"] for name, _ in REL_SCHEMA}
+        tabs.append((cols, d[f"tab{t}_pool"].tolist()))
+    preds = []
+    for line in d["sel_preds"].tolist():
+        c, op, v = line.split("\t")
+        preds.append((c, op, decode_const(v)))
+    sel = {(t, i): d[f"sel{t}_{i}"] for t in range(len(tabs)) for i in range(len(preds))}
+    joins = []
+    for j in range(int(d["n_joins"][0])):
+        a, b, key = d[f"join{j}_spec"].tolist()
+        rec = {"left": a, "right": b, "key": "kxs"[key], "n": int(d[f"join{j}_n"][0]),
+               "names": d[f"join{j}_names"].tolist()}
+        if f"join{j}_li" in d.files:
+            rec["li"], rec["ri"] = d[f"join{j}_li"], d[f"join{j}_ri"]
+        else:
+            rec["sha"] = str(d[f"join{j}_sha"][0])
+        joins.append(rec)
+    qa = {k[3:]: d[k] for k in d.files if k.startswith("qa_")}
+    return {"tables": tabs, "preds": preds, "sel": sel, "joins": joins, "qa": qa}
+
+
+def pair_digest(li, ri) -> str:
+    import hashlib
+
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(li, dtype="<i8").tobytes())
+    h.update(np.ascontiguousarray(ri, dtype="<i8").tobytes())
+    return h.hexdigest()
+
+
+def join_keys_py(cols, pool, key):
+    """Key column as python values the way the reference hashes them
+    (tables.py:408-409: decoded strings, .tolist())."""
+    col = cols[key]
+    if key == "s":
+        return [pool[c] for c in col.tolist()]
+    return col.tolist()
