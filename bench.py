@@ -513,6 +513,7 @@ def ours_arm(args):
         source = int(_ids_only(g_x)[0])
         for name, call in (("sssp", lambda: gt.sssp(g_x, source)),
                            ("connected_components", lambda: gt.connected_components(g_x)),
+                           ("scc", lambda: gt.scc(g_x)),
                            ("k_core_k8", lambda: gt.k_core(g_x, 8))):
             call()  # warm-up
             _native.profile_reset()

@@ -177,6 +177,14 @@ GT_API int gt_bfs(const gt_graph* g, int64_t source_index, int32_t* dist, int di
 GT_API int gt_connected_components(const gt_graph* g, int64_t* labels, int labels_is_device,
                                    int64_t* n_components);
 
+/* Strongly connected components (algorithms.scc, algorithms.py:144-203):
+ * labels[N] int64 aligned with the dense order, numbered in ascending order of
+ * each component's smallest id (the reference relabels its Tarjan components
+ * by first occurrence over ascending ids); *n_components (may be NULL) = their
+ * number. */
+GT_API int gt_scc(const gt_graph* g, int64_t* labels, int labels_is_device,
+                  int64_t* n_components);
+
 /* k-core (algorithms.k_core, algorithms.py:206-229): the induced subgraph
  * (graphs.py:169-183, every original edge between survivors) on the maximal
  * node set whose members keep >= k distinct undirected neighbours inside it,

@@ -442,3 +442,66 @@ def join_indices(lkeys, rkeys):
     bi = np.asarray(bi, dtype=np.int64)
     pi = np.asarray(pi, dtype=np.int64)
     return (bi, pi) if build_left else (pi, bi)
+
+
+# ------------------------------------------------------------ algorithms.scc
+
+def scc_csr(g: CSR) -> np.ndarray:
+    """algorithms.py:144-203 — iterative Tarjan over ascending ids, then dense
+    relabelling by first occurrence over ascending ids. Returns labels aligned
+    with g.ids."""
+    n = g.ids.shape[0]
+    out_off = g.out_off
+    out_adj = np.searchsorted(g.ids, g.out_adj).astype(np.int64)  # dense dst per edge
+    index = np.full(n, -1, dtype=np.int64)
+    low = np.zeros(n, dtype=np.int64)
+    on_stack = np.zeros(n, dtype=bool)
+    comp = np.full(n, -1, dtype=np.int64)
+    stack = []
+    next_index = 0
+    n_comps = 0
+    for root in range(n):
+        if index[root] >= 0:
+            continue
+        work = [(root, 0)]
+        while work:
+            v, child = work[-1]
+            if child == 0:
+                index[v] = low[v] = next_index
+                next_index += 1
+                stack.append(v)
+                on_stack[v] = True
+            a, b = int(out_off[v]), int(out_off[v + 1])
+            advanced = False
+            while child < b - a:
+                w = int(out_adj[a + child])
+                child += 1
+                if index[w] < 0:
+                    work[-1] = (v, child)
+                    work.append((w, 0))
+                    advanced = True
+                    break
+                if on_stack[w]:
+                    low[v] = min(low[v], index[w])
+            if advanced:
+                continue
+            work.pop()
+            if work:
+                parent = work[-1][0]
+                low[parent] = min(low[parent], low[v])
+            if low[v] == index[v]:
+                while True:
+                    w = stack.pop()
+                    on_stack[w] = False
+                    comp[w] = n_comps
+                    if w == v:
+                        break
+                n_comps += 1
+    remap = {}
+    labels = np.empty(n, dtype=np.int64)
+    for i in range(n):
+        c = int(comp[i])
+        if c not in remap:
+            remap[c] = len(remap)
+        labels[i] = remap[c]
+    return labels

@@ -51,6 +51,7 @@ SIGNATURES = {
     "gt_bfs": (ctypes.c_int, [_VP, ctypes.c_int64, _VP, ctypes.c_int]),
     "gt_connected_components": (ctypes.c_int, [_VP, _VP, ctypes.c_int, _I64P]),
     "gt_kcore": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.POINTER(_VP)]),
+    "gt_scc": (ctypes.c_int, [_VP, _VP, ctypes.c_int, _I64P]),
     "gt_rmat_generate": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
                                         ctypes.c_int, _VP, _VP]),
@@ -270,6 +271,15 @@ def connected_components(handle: int, n: int):
     count = ctypes.c_int64()
     check(lib.gt_connected_components(handle, _ptr(labels) if n else None, 0, ctypes.byref(count)),
           "gt_connected_components")
+    return labels, int(count.value)
+
+
+def scc(handle: int, n: int):
+    """-> (labels[N] int64, number of strongly connected components)."""
+    lib = ensure_init()
+    labels = host_empty(n, np.int64)
+    count = ctypes.c_int64()
+    check(lib.gt_scc(handle, _ptr(labels) if n else None, 0, ctypes.byref(count)), "gt_scc")
     return labels, int(count.value)
 
 

@@ -209,6 +209,17 @@ def connected_components(g) -> LabelMap:
     return LabelMap(ids, labels)
 
 
+def scc(g) -> LabelMap:
+    """Strongly connected components (algorithms.py:144-203); labels dense,
+    numbered in ascending order of each component's smallest node id."""
+    if g.node_count == 0:
+        return LabelMap(np.empty(0, np.int64), np.empty(0, np.int64))
+    dg = upload(g)
+    labels, _ = _native.scc(dg.handle, dg.node_count)
+    ids = dg.csr().ids if dg._host is not None else _ids_only(dg)
+    return LabelMap(ids, labels)
+
+
 def k_core(g, k: int) -> DeviceGraph:
     """Maximal subgraph whose nodes all have >= k distinct undirected
     neighbors (iterative peeling); the induced subgraph as a new graph."""

@@ -32,6 +32,17 @@ def golden_traverse() -> dict:
     return out
 
 
+@lru_cache(maxsize=1)
+def golden_scc() -> dict:
+    """{case: {src, dst, extra, ids, scc}} recorded from the real reference's
+    graphtables.scc (tests/golden/make_golden_scc.py)."""
+    data = np.load(GOLDEN / "scc.npz")
+    out = {}
+    for name in data["__names__"].tolist():
+        out[name] = {k.split("/", 1)[1]: data[k] for k in data.files if k.startswith(name + "/")}
+    return out
+
+
 def golden_c1() -> dict:
     data = np.load(GOLDEN / "c1.npz")
     return {k: data[k] for k in data.files}

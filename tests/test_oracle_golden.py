@@ -100,3 +100,18 @@ def test_oracle_k_core_rejects_k0():
     g = ref.build_csr([0], [1])
     with pytest.raises(ValueError):
         ref.k_core_csr(g, 0)
+
+
+# ---- scc ---------------------------------------------
+
+SCC_CASES = sorted(__import__("helpers").golden_scc())
+
+
+@pytest.mark.parametrize("name", SCC_CASES)
+def test_oracle_scc_matches_reference(name):
+    from helpers import golden_scc
+
+    case = golden_scc()[name]
+    g = _traverse_csr(case)
+    assert np.array_equal(g.ids, case["ids"])
+    assert np.array_equal(ref.scc_csr(g), case["scc"])
