@@ -527,6 +527,27 @@ def ours_arm(args):
             _native.profile_enable(False)
             extras[name] = {"ms": wall * 1e3, "kernel_ms": kern,
                             "value": g_x.edge_count / wall, "unit": "edges/s (E / call time)"}
+        # batched dynamic update: delete 1% of the rows' edges, add 1% new rows
+        k_up = max(1, rows // 100)
+        gen = torch.Generator(device=src.device).manual_seed(11)
+        pick = torch.randint(0, rows, (k_up,), device=src.device, generator=gen)
+        dels = (src[pick], dst[pick])
+        adds = (src[torch.randint(0, rows, (k_up,), device=src.device, generator=gen)],
+                dst[torch.randint(0, rows, (k_up,), device=src.device, generator=gen)])
+        _native.profile_reset()
+        _native.profile_enable(True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            g_x.apply_updates(add=adds, delete=dels)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) / args.steps
+        kern = sum(v[0] for v in _native.profile_read().values()) / args.steps
+        _native.profile_enable(False)
+        extras["update_batch"] = {"ms": wall * 1e3, "kernel_ms": kern, "added": k_up,
+                                  "deleted": k_up, "edges": g_x.edge_count,
+                                  "value": g_x.edge_count / wall,
+                                  "unit": "graph edges/s (apply_updates call time, rebuild)"}
         del g_x
         extras.update(relational_extras(table, rows, args, pk))
         if not args.no_tsv:

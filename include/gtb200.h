@@ -191,6 +191,17 @@ GT_API int gt_scc(const gt_graph* g, int64_t* labels, int labels_is_device,
  * as a new graph (free with gt_graph_free). GT_EINVAL for k < 1. */
 GT_API int gt_kcore(const gt_graph* g, int k, gt_graph** out);
 
+/* Batched dynamic update (graphs.py:92-144) into a new graph (*out; free with
+ * gt_graph_free; g is unchanged). The batch means these reference calls in
+ * this order: del_node(x) for x in d_del_nodes; del_edge(s, d) for the
+ * deletion pairs; add_node(x) for x in d_add_nodes; add_edge(s, d) for the
+ * addition pairs. Ids that are absent are ignored as the reference's calls
+ * ignore them. All arrays are device int64. */
+GT_API int gt_graph_update(const gt_graph* g, const int64_t* d_add_src, const int64_t* d_add_dst,
+                           int64_t n_add, const int64_t* d_del_src, const int64_t* d_del_dst,
+                           int64_t n_del, const int64_t* d_add_nodes, int64_t n_add_nodes,
+                           const int64_t* d_del_nodes, int64_t n_del_nodes, gt_graph** out);
+
 /* ---- relational operators feeding ToGraph -------- */
 
 /* Predicate comparison codes (tables.py:32-39 _COMPARATORS). */

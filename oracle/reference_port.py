@@ -505,3 +505,26 @@ def scc_csr(g: CSR) -> np.ndarray:
             remap[c] = len(remap)
         labels[i] = remap[c]
     return labels
+
+
+# ------------------------------------------- graphs.py:92-144 batched mutation
+
+def update_csr(g: CSR, add=None, delete=None, add_nodes=(), del_nodes=()) -> CSR:
+    """The reference's del_node* -> del_edge* -> add_node* -> add_edge* calls
+    (graphs.py:92-144) on the graph `g`, restated on edge sets: nodes minus
+    del_nodes, edges minus those incident to them and minus `delete`, then
+    add_nodes and the endpoints + edges of `add` (duplicates collapse)."""
+    src = np.repeat(g.ids, np.diff(g.out_off))
+    dst = g.out_adj
+    dead = set(int(x) for x in np.asarray(del_nodes, np.int64).tolist())
+    gone = set(zip(*(np.asarray(a, np.int64).tolist() for a in delete))) if delete else set()
+    edges = [(a, b) for a, b in zip(src.tolist(), dst.tolist())
+             if a not in dead and b not in dead and (a, b) not in gone]
+    nodes = [x for x in g.ids.tolist() if x not in dead]
+    nodes += [int(x) for x in np.asarray(add_nodes, np.int64).tolist()]
+    if add:
+        edges += list(zip(*(np.asarray(a, np.int64).tolist() for a in add)))
+    s = np.asarray([a for a, _ in edges], np.int64)
+    d = np.asarray([b for _, b in edges], np.int64)
+    out = build_csr(s, d, workers=1)
+    return add_isolated(out, np.asarray(nodes, np.int64)) if nodes else out

@@ -52,6 +52,9 @@ SIGNATURES = {
     "gt_connected_components": (ctypes.c_int, [_VP, _VP, ctypes.c_int, _I64P]),
     "gt_kcore": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.POINTER(_VP)]),
     "gt_scc": (ctypes.c_int, [_VP, _VP, ctypes.c_int, _I64P]),
+    "gt_graph_update": (ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int64, _VP, _VP, ctypes.c_int64,
+                                       _VP, ctypes.c_int64, _VP, ctypes.c_int64,
+                                       ctypes.POINTER(_VP)]),
     "gt_rmat_generate": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
                                         ctypes.c_int, _VP, _VP]),
@@ -281,6 +284,17 @@ def scc(handle: int, n: int):
     count = ctypes.c_int64()
     check(lib.gt_scc(handle, _ptr(labels) if n else None, 0, ctypes.byref(count)), "gt_scc")
     return labels, int(count.value)
+
+
+def graph_update(handle: int, add_src, add_dst, n_add: int, del_src, del_dst, n_del: int,
+                 add_nodes, n_add_nodes: int, del_nodes, n_del_nodes: int) -> int:
+    """Device pointers in -> handle of the updated graph (caller owns it)."""
+    lib = ensure_init()
+    out = _VP()
+    check(lib.gt_graph_update(handle, add_src, add_dst, int(n_add), del_src, del_dst, int(n_del),
+                              add_nodes, int(n_add_nodes), del_nodes, int(n_del_nodes),
+                              ctypes.byref(out)), "gt_graph_update")
+    return out.value or 0
 
 
 def kcore(handle: int, k: int) -> int:

@@ -250,6 +250,18 @@ def _mutating(name):
     return method
 
 
+def _as_list(a):
+    if a is None:
+        return []
+    return [int(x) for x in (a.tolist() if hasattr(a, "tolist") else a)]
+
+
+def _pair_lists(p):
+    if p is None:
+        return [], []
+    return _as_list(p[0]), _as_list(p[1])
+
+
 class DeviceGraph(_GraphReadAPI):
     """Directed simple graph whose CSR pair lives in HBM (gt_graph handle)."""
 
@@ -370,6 +382,57 @@ class DeviceGraph(_GraphReadAPI):
             self._graph = g
             self._finalizer()  # release the device CSR now
         return self._graph
+
+    def apply_updates(self, add=None, delete=None, add_nodes=None, del_nodes=None) -> None:
+        """Batched mutation on the device (gt_graph_update): the same result as
+        the reference's calls (graphs.py:92-144) del_node(x) for x in
+        del_nodes, del_edge(s, d) for (s, d) in delete, add_node(x) for x in
+        add_nodes, add_edge(s, d) for (s, d) in add — in that order. ``add``
+        and ``delete`` are (src ids, dst ids) pairs of equal-length arrays
+        (host or device). The graph stays device-resident; a graph already
+        mutated on the host applies the calls to its host records instead."""
+        if self._graph is not None:
+            g = self._graph
+            for x in _as_list(del_nodes):
+                g.del_node(x)
+            for a, b in zip(*_pair_lists(delete)):
+                g.del_edge(a, b)
+            for x in _as_list(add_nodes):
+                g.add_node(x)
+            for a, b in zip(*_pair_lists(add)):
+                g.add_edge(a, b)
+            return
+        import torch
+
+        dev = torch.device("cuda", _native.device_ordinal())
+
+        def col(a):
+            if a is None:
+                return torch.empty(0, dtype=torch.int64, device=dev)
+            if isinstance(a, torch.Tensor):
+                return a.to(device=dev, dtype=torch.int64).contiguous()
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64)).to(dev)
+
+        def pair(p):
+            if p is None:
+                return col(None), col(None)
+            a, b = col(p[0]), col(p[1])
+            if a.shape[0] != b.shape[0]:
+                raise ValueError("src and dst arrays of an update differ in length")
+            return a, b
+
+        asrc, adst = pair(add)
+        dsrc, ddst = pair(delete)
+        an, dn = col(add_nodes), col(del_nodes)
+        ptr = lambda t: t.data_ptr() if t.numel() else None  # noqa: E731
+        new = _native.graph_update(self.handle, ptr(asrc), ptr(adst), asrc.shape[0],
+                                   ptr(dsrc), ptr(ddst), dsrc.shape[0], ptr(an), an.shape[0],
+                                   ptr(dn), dn.shape[0])
+        self._finalizer()
+        self._handle = new
+        self._n, self._e = _native.graph_sizes(new)
+        self._host = None
+        self._finalizer = weakref.finalize(self, _native.graph_free, new)
 
     add_node = _mutating("add_node")
     add_edge = _mutating("add_edge")

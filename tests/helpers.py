@@ -43,6 +43,18 @@ def golden_scc() -> dict:
     return out
 
 
+@lru_cache(maxsize=1)
+def golden_updates() -> dict:
+    """{case: {src, dst, del_nodes, del_src, del_dst, add_nodes, add_src,
+    add_dst, ids, out_off, out_adj, in_off, in_adj}} from the real reference's
+    Graph mutation calls (tests/golden/make_golden_updates.py)."""
+    data = np.load(GOLDEN / "updates.npz")
+    out = {}
+    for name in data["__names__"].tolist():
+        out[name] = {k.split("/", 1)[1]: data[k] for k in data.files if k.startswith(name + "/")}
+    return out
+
+
 def golden_c1() -> dict:
     data = np.load(GOLDEN / "c1.npz")
     return {k: data[k] for k in data.files}

@@ -115,3 +115,20 @@ def test_oracle_scc_matches_reference(name):
     g = _traverse_csr(case)
     assert np.array_equal(g.ids, case["ids"])
     assert np.array_equal(ref.scc_csr(g), case["scc"])
+
+
+# ---- batched dynamic updates ---------------------------
+
+UPDATE_CASES = sorted(__import__("helpers").golden_updates())
+
+
+@pytest.mark.parametrize("name", UPDATE_CASES)
+def test_oracle_updates_match_reference(name):
+    from helpers import golden_updates
+
+    c = golden_updates()[name]
+    g = ref.build_csr(c["src"], c["dst"], workers=1)
+    got = ref.update_csr(g, add=(c["add_src"], c["add_dst"]), delete=(c["del_src"], c["del_dst"]),
+                         add_nodes=c["add_nodes"], del_nodes=c["del_nodes"])
+    for f in ("ids", "out_off", "out_adj", "in_off", "in_adj"):
+        assert np.array_equal(getattr(got, f), c[f]), f
