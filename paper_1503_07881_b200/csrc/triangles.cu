@@ -718,6 +718,92 @@ __global__ void __launch_bounds__(256) place_rows_kernel(
   }
 }
 
+// Arc-parallel version of place_rows_kernel: 2048-arc tiles of the
+// rank-space CSR, the tile's rows staged in shared memory (start, buffer
+// base) with the slot -> row map built like cand_degree_kernel's. Each thread
+// handles 8 arcs and has all 8 N-(v) slot claims (returning atomics) in
+// flight at once, where the warp-per-row kernel waited on one claim per lane
+// per row (latency-bound: rows average ~30 arcs).
+__global__ void __launch_bounds__(256) place_tiles_kernel(
+    const int64_t* __restrict__ off_p, const int64_t* __restrict__ tile_row, int64_t m,
+    const int32_t* __restrict__ order, const int64_t* __restrict__ und_off,
+    const int32_t* __restrict__ buf, const int64_t* __restrict__ off_m,
+    int32_t* __restrict__ adj_p, unsigned int* __restrict__ cur, int2* __restrict__ nm) {
+  constexpr int T = TC_CAND_TILE, PER = T / 256;
+  __shared__ int32_t s_c[TC_ROWS_CAP];                 // off_p[r0 + i] - e0
+  __shared__ int64_t s_b[TC_ROWS_CAP];                 // und_off[order[r0 + i]]
+  __shared__ __align__(16) int32_t s_row[T];           // slot -> row - r0
+  __shared__ int32_t s_wmax[8];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t e0 = int64_t(blockIdx.x) * T;
+  const int64_t r0 = tile_row[blockIdx.x], r1 = tile_row[blockIdx.x + 1];
+  const int64_t nr = r1 - r0 + 2;
+  const bool staged = nr <= TC_ROWS_CAP;
+  const int tn = int(m - e0 < T ? m - e0 : int64_t(T));
+  if (staged) {
+    for (int i = tid; i < int(nr); i += 256) {
+      s_c[i] = int32_t(off_p[r0 + i] - e0);
+      if (i < int(nr) - 1) s_b[i] = und_off[order[r0 + i]];
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) s_row[q * 256 + tid] = 0;
+    __syncthreads();
+    for (int i = tid + 1; i < int(nr) - 1; i += 256) {
+      const int32_t c = s_c[i];
+      if (c < T && s_c[i + 1] > c) s_row[c] = i;
+    }
+    __syncthreads();
+    int4 a = reinterpret_cast<int4*>(s_row)[2 * tid];
+    int4 b = reinterpret_cast<int4*>(s_row)[2 * tid + 1];
+    a.y = max(a.y, a.x); a.z = max(a.z, a.y); a.w = max(a.w, a.z);
+    b.x = max(b.x, a.w); b.y = max(b.y, b.x); b.z = max(b.z, b.y); b.w = max(b.w, b.z);
+    int run = b.w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, run, o);
+      if (lane >= o) run = max(run, y);
+    }
+    if (lane == 31) s_wmax[warp] = run;
+    int excl = __shfl_up_sync(0xffffffffu, run, 1);
+    if (lane == 0) excl = 0;
+    __syncthreads();
+    for (int w = 0; w < warp; ++w) excl = max(excl, s_wmax[w]);
+    a.x = max(a.x, excl); a.y = max(a.y, excl); a.z = max(a.z, excl); a.w = max(a.w, excl);
+    b.x = max(b.x, excl); b.y = max(b.y, excl); b.z = max(b.z, excl); b.w = max(b.w, excl);
+    reinterpret_cast<int4*>(s_row)[2 * tid] = a;
+    reinterpret_cast<int4*>(s_row)[2 * tid + 1] = b;
+  } else {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int t = q * 256 + tid;
+      if (t < tn) s_row[t] = int32_t(row_of(off_p, r0, r1, e0 + t) - r0);
+    }
+  }
+  __syncthreads();
+  int32_t v[PER], rem[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int t = q * 256 + tid;
+    v[q] = -1;
+    if (t < tn) {
+      const int ri = s_row[t];
+      const int64_t c = staged ? s_c[ri] : off_p[r0 + ri] - e0;
+      const int64_t c1 = staged ? s_c[ri + 1] : off_p[r0 + ri + 1] - e0;
+      const int64_t base = staged ? s_b[ri] : und_off[order[r0 + ri]];
+      const int64_t k = t - c;
+      v[q] = buf[base + k];
+      rem[q] = int32_t(c1 - t - 1);
+      adj_p[e0 + t] = v[q];
+    }
+  }
+  unsigned int slot[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) slot[q] = v[q] >= 0 ? atomicAdd(&cur[v[q]], 1u) : 0u;
+#pragma unroll
+  for (int q = 0; q < PER; ++q)
+    if (v[q] >= 0) nm[off_m[v[q]] + slot[q]] = make_int2(int(e0 + q * 256 + tid + 1), rem[q]);
+}
+
 // ---- work lists --------------------------------------------------------------
 // kind 0: warp bitmap tasks (n-1-v <= TC_BM_BITS), 3: warp split tasks
 // (d+(v) <= TC_SPLIT_MAX), 1: warp hash tasks, 2: CTA hash tasks. A task is (v, chunk of N-(v)); it needs d+(v), d-(v) >= 1.
@@ -1391,8 +1477,14 @@ static Oriented orient(const gt_graph* g) {
   {
     Phase ph("tc.oriented_csr", 8.0 * o.m + 4.0 * o.m + 4.0 * o.m + 8.0 * o.m + 8.0 * n);
     GT_CUDA(cudaMemsetAsync(cur, 0, size_t(n) * 4, s));
-    GT_LAUNCH(gtd::place_rows_kernel, grid_cap(ceil_div64(n, 8)), 256, 0, order, und_off, dplus,
-              buf, n, o.off_p, o.off_m, o.adj_p, cur, o.nm);
+    if (o.m > 0) {
+      const int64_t tiles = ceil_div64(o.m, gtd::TC_CAND_TILE);
+      int64_t* tile_row = ws_n<int64_t>(WS_KEYS_A, size_t(tiles) + 1);  // sorts are done
+      GT_LAUNCH(gtd::cand_tile_rows_kernel, ceil_div(tiles + 1, 256), 256, 0, o.off_p, n, o.m,
+                tiles, tile_row);
+      GT_LAUNCH(gtd::place_tiles_kernel, static_cast<int>(tiles), 256, 0, o.off_p, tile_row, o.m,
+                order, und_off, buf, o.off_m, o.adj_p, cur, o.nm);
+    }
   }
   return o;
 }
