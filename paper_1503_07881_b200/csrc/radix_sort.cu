@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MIN_BLOCKS)
                     int shift, const int64_t* __restrict__ digit_base,
                     uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter,
                     uint32_t epoch) {
-  __shared__ OnesweepSmem s;
+  extern __shared__ __align__(16) unsigned char os_dsm[];  // dynamic: tiles may exceed 48 KB
+  OnesweepSmem& s = *reinterpret_cast<OnesweepSmem*>(os_dsm);
   if (threadIdx.x == 0) s.tile = atomicAdd(tile_counter, 1u);
   for (int i = threadIdx.x; i < (RS_THREADS / 32) * 256; i += RS_THREADS) (&s.whist[0][0])[i] = 0;
   __syncthreads();
@@ -260,8 +261,15 @@ template <int BITS, int M>
 static void launch_bits(int grid, const uint64_t* src, uint64_t* dst, int64_t n, int shift,
                         const int64_t* digit_base, uint64_t* status, uint32_t* counter,
                         uint32_t epoch) {
-  GT_LAUNCH((gtd::onesweep_kernel<BITS, M>), grid, RS_THREADS, 0, src, dst, n, shift, digit_base,
-            status, counter, epoch);
+  static bool attr_set = false;
+  if (!attr_set) {
+    GT_CUDA(cudaFuncSetAttribute(gtd::onesweep_kernel<BITS, M>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(sizeof(gtd::OnesweepSmem))));
+    attr_set = true;
+  }
+  GT_LAUNCH((gtd::onesweep_kernel<BITS, M>), grid, RS_THREADS, sizeof(gtd::OnesweepSmem), src, dst,
+            n, shift, digit_base, status, counter, epoch);
 }
 
 template <int M>
