@@ -51,6 +51,8 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-rows", type=int, default=1_000_000)
     p.add_argument("--no-tsv", action="store_true")
+    p.add_argument("--no-extras", action="store_true",
+                   help="skip the measured-apart extras (SURVEY 8f rows): step kernels only")
     p.add_argument("--tsv-rows", type=int, default=4_000_000)
     p.add_argument("--sharded", action="store_true",
                    help="use the multi-GPU (distributed.py) pipeline even on one GPU")
@@ -491,7 +493,7 @@ def ours_arm(args):
 
     # ---- §8f next #1: graph -> edge table export (device), measured apart ----
     extras = {}
-    if not sharded:
+    if not sharded and not args.no_extras:
         g_x = gt.table_to_graph(table, edge_spec)
         _native.profile_reset()
         _native.profile_enable(True)
