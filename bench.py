@@ -45,7 +45,7 @@ def parse_args():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", choices=["c1", "c2", "c4"], default="c2")
+    p.add_argument("--config", choices=["c1", "c2", "c4", "c5"], default="c2")
     p.add_argument("--iterations", type=int, default=20)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -86,20 +86,36 @@ def spec_for(name):
     return CONFIGS[name]
 
 
+def has_tc(spec):
+    """C5 (uniform, BASELINE configs[4]) is ToGraph + PageRank only."""
+    from paper_1503_07881_b200.synth import UniformSpec
+
+    return not isinstance(spec, UniformSpec)
+
+
+def spec_desc(name, spec, rows):
+    from paper_1503_07881_b200.synth import UniformSpec
+
+    if isinstance(spec, UniformSpec):
+        return (f"{name}: uniform iid (Erdos-Renyi) {rows} rows over {spec.n_nodes} ids "
+                f"seed {spec.seed}")
+    return f"{name}: R-MAT s{spec.scale} {rows} rows seed {spec.seed} permuted={spec.permute}"
+
+
 # ------------------------------------------------------------------ reference
 
 def run_cpu_sample(spec, rows, iterations):
     """The reference algorithm (oracle port, all host cores) on rows [0, rows)."""
     from oracle import reference_port as ref
-    from paper_1503_07881_b200.synth import rmat_edges
+    from paper_1503_07881_b200.synth import spec_edges
 
-    src, dst = rmat_edges(spec.scale, rows, spec.a, spec.b, spec.c, spec.seed, spec.permute)
+    src, dst = spec_edges(spec, rows)
     t0 = time.perf_counter()
     g = ref.build_csr(src, dst)
     t1 = time.perf_counter()
     ref.pagerank_csr(g, 0.85, iterations)
     t2 = time.perf_counter()
-    tc = ref.triangle_count_csr(g)
+    tc = ref.triangle_count_csr(g) if has_tc(spec) else None
     t3 = time.perf_counter()
     return {"rows": rows, "n": g.n, "e": g.e, "tc": tc, "build_s": t1 - t0, "pr_s": t2 - t1,
             "tc_s": t3 - t2, "total_s": t3 - t0}
@@ -133,8 +149,8 @@ def reference_arm(args):
     mean = sum(times) / len(times)
     value = rows / mean
     info = cpu_info()
-    sample = (f"rows [0,{rows}) of {args.config} (R-MAT s{spec.scale}, seed {spec.seed}, "
-              f"permuted={spec.permute}): build + PageRank x{args.iterations} + triangles; "
+    sample = (f"rows [0,{rows}) of {spec_desc(args.config, spec, spec.rows)}: build + PageRank "
+              f"x{args.iterations}{' + triangles' if has_tc(spec) else ''}; "
               f"N={last['n']} E={last['e']}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s",
@@ -386,6 +402,7 @@ def ours_arm(args):
     state = {}
 
     sharded = world > 1 or args.sharded
+    with_tc = has_tc(spec)
     if sharded and not dist_ready():
         import torch.distributed as dist
 
@@ -399,7 +416,7 @@ def ours_arm(args):
             if out is None or out.shape[0] != g.node_count:
                 out = state["scores"] = torch.empty(g.node_count, dtype=torch.float64, device=dev)
             gt.pagerank_device(g, 0.85, iters, out.data_ptr())
-            tc = gt.triangle_count(g)
+            tc = gt.triangle_count(g) if with_tc else None
             state.update(n=g.node_count, e=g.edge_count, tc=tc)
             del g
     else:
@@ -410,7 +427,7 @@ def ours_arm(args):
         def step():
             sg = D.build_csr(src, dst, ops=ops)
             D.pagerank(sg, 0.85, iters, ops=ops)
-            tc = D.triangle_count(sg, ops=ops)
+            tc = D.triangle_count(sg, ops=ops) if with_tc else None
             state.update(n=sg.n, e=sg.e, tc=tc)
             del sg
 
@@ -574,7 +591,7 @@ def ours_arm(args):
                 t1_ = time.perf_counter()
                 pr = gt.pagerank(g, 0.85, iters)
                 t2_ = time.perf_counter()
-                tc_ = gt.triangle_count(g)
+                tc_ = gt.triangle_count(g) if with_tc else None
                 if os.environ.get("BENCH_E2E_DEBUG"):
                     print(f"e2e split: build {1e3 * (t1_ - t0_):.1f} pr {1e3 * (t2_ - t1_):.1f} "
                           f"tc {1e3 * (time.perf_counter() - t2_):.1f} ms", file=sys.stderr)
@@ -585,7 +602,7 @@ def ours_arm(args):
                 d_d = h_dst.to(dev, non_blocking=True)
                 sg = D.build_csr(s_d, d_d, ops=ops)
                 pr = D.pagerank(sg, 0.85, iters, ops=ops).cpu()
-                tc_ = D.triangle_count(sg, ops=ops)
+                tc_ = D.triangle_count(sg, ops=ops) if with_tc else None
                 return pr, tc_
 
         # warm-up in the timed loop's pattern (the previous step's result
@@ -617,7 +634,8 @@ def ours_arm(args):
         e2e = {"value": rows * world / (e2e_ms / 1e3), "unit": "rows/s",
                "ms_per_step": e2e_ms, "h2d_bytes_per_step": 16 * rows,
                "d2h_bytes_per_step": 16 * n + 8 + 8,
-               "api": "table_to_graph(host ColumnTable) -> pagerank -> triangle_count"}
+               "api": "table_to_graph(host ColumnTable) -> pagerank"
+                      f"{' -> triangle_count' if with_tc else ''}"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -625,8 +643,9 @@ def ours_arm(args):
         info = cpu_info()
         cpu = {"value": r["rows"] / r["total_s"], "unit": "rows/s", "cores": info["cores"],
                "kind": "port",
-               "sample": (f"rows [0,{r['rows']}) of {args.config}: build + PageRank x{iters} + "
-                          f"triangles via oracle/reference_port.py (numpy, workers=all cores), "
+               "sample": (f"rows [0,{r['rows']}) of {args.config}: build + PageRank x{iters}"
+                          f"{' + triangles' if with_tc else ''} via oracle/reference_port.py "
+                          f"(numpy, workers=all cores), "
                           f"N={r['n']} E={r['e']}; {r['total_s']:.2f}s"),
                "cpu": info["model"],
                "phases_s": {k: r[k] for k in ("build_s", "pr_s", "tc_s")}}
@@ -635,10 +654,10 @@ def ours_arm(args):
         "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "int64+f64", "data": "synthetic (R-MAT generated on device, seeded)",
-        "config": {"workload": f"{args.config}: R-MAT s{spec.scale} {rows * world} rows seed {spec.seed}"
-                               f" permuted={spec.permute}; ToGraph + PageRank x{iters} fp64 + "
-                               "triangles (C3)",
+        "dtype": "int64+f64", "data": "synthetic (generated on device, seeded)",
+        "config": {"workload": f"{spec_desc(args.config, spec, rows * world)}; ToGraph + "
+                               f"PageRank x{iters} fp64"
+                               f"{' + triangles (C3)' if with_tc else ''}",
                    "rows": rows, "nodes": n, "edges": e, "triangles": tc,
                    "pagerank_iterations": iters,
                    "parallelism": f"sharded x{world} (NCCL)" if sharded else "single",

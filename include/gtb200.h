@@ -255,6 +255,14 @@ GT_API int gt_rmat_generate_range(int scale, int64_t start, int64_t rows, double
                                   double c, uint64_t seed, int permute, int64_t* d_src,
                                   int64_t* d_dst);
 
+/* Uniform rows (the stand-in for BASELINE config 4, synth.random_edges
+ * semantics: src, dst iid uniform in [0, n_nodes)), bit-identical to the numpy
+ * generator paper_1503_07881_b200.synth.uniform_edges: row e uses
+ * hi64(splitmix64(key + 2e) * n) for src and key + 2e + 1 for dst,
+ * key = splitmix64(seed ^ 0xD1B54A32D192ED03). */
+GT_API int gt_uniform_generate_range(int64_t n_nodes, int64_t start, int64_t rows, uint64_t seed,
+                                     int64_t* d_src, int64_t* d_dst);
+
 /* ---- multi-GPU primitives ------------------------------------------------
  * One process per GPU; paper_1503_07881_b200/distributed.py runs the
  * collectives (torch.distributed / NCCL) between these calls. They are the

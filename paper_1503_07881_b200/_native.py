@@ -61,6 +61,8 @@ SIGNATURES = {
     "gt_rmat_generate_range": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
                                               ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                               ctypes.c_uint64, ctypes.c_int, _VP, _VP]),
+    "gt_uniform_generate_range": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                                 ctypes.c_uint64, _VP, _VP]),
     "gt_id_minmax": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, _VP]),
     "gt_id_presence": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                       _VP]),
@@ -368,6 +370,12 @@ def graph_node_table(handle: int, node, out_deg, in_deg):
     lib = ensure_init()
     check(lib.gt_graph_node_table(handle, _ptr(node), _ptr(out_deg), _ptr(in_deg), 0),
           "gt_graph_node_table")
+
+
+def uniform_generate(n_nodes, rows, seed, src_ptr, dst_ptr, start=0):
+    lib = ensure_init()
+    check(lib.gt_uniform_generate_range(int(n_nodes), int(start), int(rows), int(seed),
+                                        int(src_ptr), int(dst_ptr)), "gt_uniform_generate_range")
 
 
 def rmat_generate(scale, rows, a, b, c, seed, permute, src_ptr, dst_ptr, start=0):

@@ -66,9 +66,41 @@ __global__ void __launch_bounds__(256) rmat_kernel(int64_t start, int64_t rows, 
   }
 }
 
+// Uniform (Erdős–Rényi) rows, the stand-in for BASELINE config 4's
+// synth.random_edges table (numpy twin: synth.uniform_edges):
+//   key = splitmix64(seed ^ 0xD1B54A32D192ED03)
+//   src = hi64(splitmix64(key + 2e) * n),  dst = hi64(splitmix64(key + 2e + 1) * n)
+__global__ void __launch_bounds__(256) uniform_kernel(int64_t start, int64_t rows, uint64_t key,
+                                                      uint64_t n, int64_t* __restrict__ src,
+                                                      int64_t* __restrict__ dst) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows; e += stride) {
+    const uint64_t b = key + 2ull * uint64_t(start + e);
+    src[e] = int64_t(__umul64hi(splitmix64(b), n));
+    dst[e] = int64_t(__umul64hi(splitmix64(b + 1ull), n));
+  }
+}
+
 }  // namespace gtd
 
 using namespace gt;
+
+extern "C" int gt_uniform_generate_range(int64_t n_nodes, int64_t start, int64_t rows,
+                                         uint64_t seed, int64_t* d_src, int64_t* d_dst) {
+  GT_API_BEGIN
+  require_init();
+  if (n_nodes < 1 || rows < 0 || start < 0) fail(GT_EINVAL, "need n_nodes >= 1, rows >= 0");
+  if (rows == 0) return GT_OK;
+  if (!d_src || !d_dst) fail(GT_EINVAL, "output pointers must not be NULL");
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div64(rows, 256), 16LL * ctx().sm_count));
+  {
+    Phase ph("synth.uniform", 16.0 * rows);
+    GT_LAUNCH(gtd::uniform_kernel, grid, 256, 0, start, rows,
+              gtd::splitmix64(seed ^ 0xD1B54A32D192ED03ull), uint64_t(n_nodes), d_src, d_dst);
+  }
+  sync();
+  GT_API_END
+}
 
 extern "C" int gt_rmat_generate_range(int scale, int64_t start, int64_t rows, double a, double b,
                                       double c, uint64_t seed, int permute, int64_t* d_src,

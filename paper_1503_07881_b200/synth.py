@@ -112,17 +112,62 @@ def random_edges_arrays(n_nodes: int, n_edges: int, seed: int = 0):
     return src, dst
 
 
-# BASELINE.json configs (C3 reuses the C2 table; C4's dense remap and C5's
-# 2B-row uniform table are generated on the device by bench.py).
+_UNIFORM_SALT = 0xD1B54A32D192ED03
+
+
+def _mulhi64(x: np.ndarray, n: int) -> np.ndarray:
+    """High 64 bits of x * n for uint64 x and n < 2^32 (no 128-bit numpy ints)."""
+    xh = x >> _U64(32)
+    xl = x & _U64(0xFFFFFFFF)
+    nn = _U64(n)
+    return (xh * nn + ((xl * nn) >> _U64(32))) >> _U64(32)
+
+
+def uniform_edges(n_nodes: int, rows: int, seed: int = 4, start: int = 0):
+    """Uniform iid (src, dst) in [0, n_nodes): the counter-based stand-in for
+    BASELINE config 4 (reference synth.random_edges semantics, synth.py:20-29),
+    bit-identical to csrc/rmat.cu uniform_kernel. Row e: src =
+    hi64(splitmix64(key + 2e) * n), dst from key + 2e + 1."""
+    if not 1 <= n_nodes < (1 << 32):
+        raise ValueError("n_nodes must be in [1, 2^32)")
+    key = _sm64_scalar(seed ^ _UNIFORM_SALT)
+    e = np.arange(start, start + rows, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        b = _U64(key) + _U64(2) * e
+        src = _mulhi64(splitmix64(b), n_nodes).astype(np.int64)
+        dst = _mulhi64(splitmix64(b + _U64(1)), n_nodes).astype(np.int64)
+    return src, dst
+
+
+@dataclass(frozen=True)
+class UniformSpec:
+    n_nodes: int
+    rows: int
+    seed: int = 4
+
+
+# BASELINE.json configs (C3 reuses the C2 table; C4 and C5 are generated on
+# the device by bench.py).
 CONFIGS = {
     "c1": RmatSpec(scale=17, rows=1_048_576, seed=1, permute=False),
     "c2": RmatSpec(scale=22, rows=69_000_000, seed=2, permute=True),
     "c4": RmatSpec(scale=26, rows=1_470_000_000, seed=3, permute=True),
+    "c5": UniformSpec(n_nodes=100_000_000, rows=2_000_000_000, seed=4),
 }
 
 
-def rmat_device(spec: RmatSpec, device: str = "cuda", start: int = 0, rows: int | None = None):
-    """Generate rows [start, start+rows) of an R-MAT table straight into HBM."""
+def spec_edges(spec, rows: int | None = None, start: int = 0):
+    """Host (numpy) rows [start, start+rows) of a config's table."""
+    rows = spec.rows if rows is None else rows
+    if isinstance(spec, UniformSpec):
+        return uniform_edges(spec.n_nodes, rows, spec.seed, start)
+    assert start == 0
+    return rmat_edges(spec.scale, rows, spec.a, spec.b, spec.c, spec.seed, spec.permute)
+
+
+def rmat_device(spec, device: str = "cuda", start: int = 0, rows: int | None = None):
+    """Generate rows [start, start+rows) of a config's table (R-MAT or uniform)
+    straight into HBM."""
     import torch
 
     from . import _native
@@ -130,6 +175,10 @@ def rmat_device(spec: RmatSpec, device: str = "cuda", start: int = 0, rows: int 
     rows = spec.rows if rows is None else rows
     src = torch.empty(rows, dtype=torch.int64, device=device)
     dst = torch.empty(rows, dtype=torch.int64, device=device)
+    if isinstance(spec, UniformSpec):
+        _native.uniform_generate(spec.n_nodes, rows, spec.seed, src.data_ptr(), dst.data_ptr(),
+                                 start=start)
+        return src, dst
     _native.rmat_generate(spec.scale, rows, spec.a, spec.b, spec.c, spec.seed, spec.permute,
                           src.data_ptr(), dst.data_ptr(), start=start)
     return src, dst
