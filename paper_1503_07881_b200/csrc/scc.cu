@@ -135,6 +135,59 @@ __global__ void __launch_bounds__(256) scc_reach_kernel(
   }
 }
 
+// Top-down level for a handful of frontier nodes (the pivot's first level: one
+// hub with up to ~10^6 edges): every warp of the grid takes a slice of each
+// node's adjacency instead of one warp walking it alone.
+__global__ void __launch_bounds__(256) scc_reach_wide_kernel(
+    const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
+    const int32_t* __restrict__ q, int64_t nq, const int32_t* __restrict__ scc,
+    uint32_t* __restrict__ vis, uint32_t bit, int32_t* __restrict__ next,
+    unsigned int* __restrict__ count) {
+  const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = int64_t(gridDim.x) * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = 0; i < nq; ++i) {
+    const int32_t v = q[i];
+    const int64_t a = off[v], b = off[v + 1];
+    for (int64_t base = a + gw * 32; base < b; base += nw * 32) {
+      const int64_t e = base + lane;
+      bool app = false;
+      int32_t w = 0;
+      if (e < b) {
+        w = adj[e];
+        if (scc[w] < 0 && !(__ldcg(vis + w) & bit)) app = !(atomicOr(vis + w, bit) & bit);
+      }
+      scc_append(app, w, next, count);
+    }
+  }
+}
+
+// Bottom-up level of the same search (direction optimisation, Beamer et al.):
+// every live node not yet reached looks for a reached live neighbour along
+// the reverse adjacency and stops at the first. Reachability needs no levels,
+// so a node may also be reached through one marked earlier in this sweep.
+__global__ void __launch_bounds__(256) scc_reach_up_kernel(
+    const int64_t* __restrict__ roff, const int32_t* __restrict__ radj, int64_t n,
+    const int32_t* __restrict__ scc, uint32_t* __restrict__ vis, uint32_t bit,
+    int32_t* __restrict__ next, unsigned int* __restrict__ count) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
+    const int64_t v = base + threadIdx.x;
+    bool hit = false;
+    if (v < n && scc[v] < 0 && !(__ldcg(vis + v) & bit)) {
+      for (int64_t e = roff[v], b = roff[v + 1]; e < b; ++e) {
+        const int32_t u = radj[e];
+        if (scc[u] < 0 && (__ldcg(vis + u) & bit)) {
+          hit = true;
+          break;
+        }
+      }
+      if (hit) atomicOr(vis + v, bit);
+    }
+    scc_append(hit, int32_t(v), next, count);
+  }
+}
+
 // Forward ∩ backward of the pivot: smallest member, then assignment.
 __global__ void __launch_bounds__(256) scc_fb_min_kernel(int64_t n, const int32_t* __restrict__ scc,
                                                          const uint32_t* __restrict__ vis,
@@ -282,6 +335,11 @@ __global__ void __launch_bounds__(256) scc_label_kernel(const int32_t* __restric
 
 namespace gt {
 
+// bottom-up once the frontier exceeds n / SCC_UP_DIV nodes: on power-law
+// graphs the frontier after the pivot's first level already holds most of the
+// edges (C2: 8 top-down levels 17.1 ms vs bottom-up sweeps ~0.05 ms each)
+constexpr int64_t SCC_UP_DIV = 2048;
+
 static int scc_grid(int64_t items, int per_block) {
   return static_cast<int>(std::max<int64_t>(
       1, std::min<int64_t>(ceil_div64(items, per_block), int64_t(ctx().sm_count) * 16)));
@@ -328,16 +386,24 @@ static int64_t scc(const gt_graph* g, int64_t* out, bool out_device) {
       if (read_counter(cnt) == 0) break;
     }
   };
-  // frontier search from q0[0] over (off, adj) marking `bit`
-  auto reach = [&](const int64_t* off, const int32_t* adj, uint32_t bit, int32_t* qa,
-                   int32_t* qb) {
+  // frontier search from q0[0] over (off, adj) marking `bit`; large
+  // frontiers switch to bottom-up sweeps over the reverse adjacency
+  auto reach = [&](const int64_t* off, const int32_t* adj, const int64_t* roff,
+                   const int32_t* radj, uint32_t bit, int32_t* qa, int32_t* qb) {
     int64_t nq = 1;
     while (nq > 0) {
       GT_CUDA(cudaMemsetAsync(cnt, 0, 4, s));
       {
-        Phase ph("scc.pivot_reach", 0.0);
-        GT_LAUNCH(gtd::scc_reach_kernel, scc_grid(nq, 8), 256, 0, off, adj, qa, nq, sc, vis, bit,
-                  qb, cnt);
+        const bool up = nq > n / SCC_UP_DIV;
+        Phase ph(up ? "scc.reach_up" : "scc.reach_down", 0.0);
+        if (up)
+          GT_LAUNCH(gtd::scc_reach_up_kernel, gn, 256, 0, roff, radj, n, sc, vis, bit, qb, cnt);
+        else if (nq <= 32)
+          GT_LAUNCH(gtd::scc_reach_wide_kernel, 4 * ctx().sm_count, 256, 0, off, adj, qa, nq, sc,
+                    vis, bit, qb, cnt);
+        else
+          GT_LAUNCH(gtd::scc_reach_kernel, scc_grid(nq, 8), 256, 0, off, adj, qa, nq, sc, vis,
+                    bit, qb, cnt);
       }
       nq = read_counter(cnt);
       std::swap(qa, qb);
@@ -358,9 +424,9 @@ static int64_t scc(const gt_graph* g, int64_t* out, bool out_device) {
     int32_t* qf = q0;
     int32_t* qb = q1;
     GT_LAUNCH(gtd::scc_seed_kernel, 1, 1, 0, best, vis, qf, live);
-    reach(g->out_off, g->out_adj, 1u, qf, qb);
+    reach(g->out_off, g->out_adj, g->in_off, g->in_adj, 1u, qf, qb);
     GT_CUDA(cudaMemcpyAsync(q0, live, 4, cudaMemcpyDeviceToDevice, s));
-    reach(g->in_off, g->in_adj, 2u, q0, q1);
+    reach(g->in_off, g->in_adj, g->out_off, g->out_adj, 2u, q0, q1);
     const int big = 0x7fffffff;
     GT_CUDA(cudaMemcpyAsync(rep, &big, 4, cudaMemcpyHostToDevice, s));
     Phase ph("scc.pivot", 12.0 * n);

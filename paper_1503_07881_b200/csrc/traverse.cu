@@ -320,6 +320,9 @@ static int warps_grid(int64_t items) {
       1, std::min<int64_t>(ceil_div64(items, 8), int64_t(ctx().sm_count) * 16)));
 }
 
+// frontier size (share of n) above which a level runs bottom-up
+constexpr int64_t BFS_UP_DIV = 2048;
+
 static void bfs(const gt_graph* g, int64_t source, int32_t* out, bool out_device) {
   require_init();
   const int64_t n = g->n;
@@ -339,7 +342,7 @@ static void bfs(const gt_graph* g, int64_t source, int32_t* out, bool out_device
   // share of the graph, top-down otherwise
   while (nf > 0) {
     GT_CUDA(cudaMemsetAsync(counter, 0, 4, s));
-    const bool bottom_up = nf > n / 24 && n - visited > 0;
+    const bool bottom_up = nf > n / BFS_UP_DIV && n - visited > 0;
     {
       Phase ph(bottom_up ? "bfs.bottom_up" : "bfs.top_down", 0.0);
       if (bottom_up)
