@@ -276,34 +276,66 @@ __global__ void __launch_bounds__(256) kcore_peel_kernel(
   }
 }
 
-// Warp per row u: edges (ids[u], ids[v]) with both ends alive, appended in
-// any order (the CSR build sorts).
+// Edges (u, v) with both ends alive, as dense indices, appended in any order
+// (the CSR build sorts; dense order = id order, so the built graph only needs
+// its node list mapped back through ids). Blocks walk chunks of KC_ROWS rows twice: count the chunk's
+// kept edges (warp per row), reserve them with ONE global atomic per chunk,
+// then write them through a shared-memory cursor. (A global atomic per warp
+// step serialised ~45 M atomics on one address: 101 ms at C4.)
+constexpr int KC_ROWS = 256;
+
 __global__ void __launch_bounds__(256) kcore_edges_kernel(
     const int64_t* __restrict__ ids, const int64_t* __restrict__ off,
     const int32_t* __restrict__ adj, int64_t n, const uint8_t* __restrict__ alive,
     int64_t* __restrict__ src, int64_t* __restrict__ dst, unsigned long long* __restrict__ count) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t u = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < n; u += nwarps) {
-    if (!alive[u]) continue;  // warp-uniform
-    const int64_t a = off[u], b = off[u + 1];
-    const int64_t su = ids[u];
-    for (int64_t k0 = a; k0 < b; k0 += 32) {
-      const int64_t k = k0 + lane;
-      int32_t v = 0;
-      const bool keep = k < b && alive[v = adj[k]];
-      const unsigned bal = __ballot_sync(FULL, keep);
-      if (!bal) continue;
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(bal));
-      base = __shfl_sync(FULL, base, 0);
-      if (keep) {
-        const unsigned long long p = base + __popc(bal & lanemask_lt());
-        src[p] = su;
-        dst[p] = ids[v];
+  __shared__ unsigned long long s_cnt, s_base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t r0 = int64_t(blockIdx.x) * KC_ROWS; r0 < n; r0 += int64_t(gridDim.x) * KC_ROWS) {
+    const int64_t r1 = min(n, r0 + KC_ROWS);
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    unsigned long long mine = 0;
+    for (int64_t u = r0 + warp; u < r1; u += 8) {
+      if (!alive[u]) continue;  // warp-uniform
+      for (int64_t k = off[u] + lane, b = off[u + 1]; k < b; k += 32) mine += alive[adj[k]] ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(FULL, mine, o);
+    if (lane == 0 && mine) atomicAdd(&s_cnt, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_base = s_cnt ? atomicAdd(count, s_cnt) : 0ull;
+      s_cnt = 0;
+    }
+    __syncthreads();
+    for (int64_t u = r0 + warp; u < r1; u += 8) {
+      if (!alive[u]) continue;
+      const int64_t a = off[u], b = off[u + 1];
+      for (int64_t k0 = a; k0 < b; k0 += 32) {
+        const int64_t k = k0 + lane;
+        int32_t v = 0;
+        const bool keep = k < b && alive[v = adj[k]];
+        const unsigned bal = __ballot_sync(FULL, keep);
+        if (!bal) continue;
+        unsigned long long pos = 0;
+        if (lane == 0) pos = atomicAdd(&s_cnt, (unsigned long long)__popc(bal));
+        pos = s_base + __shfl_sync(FULL, pos, 0);
+        if (keep) {
+          const unsigned long long p = pos + __popc(bal & lanemask_lt());
+          src[p] = u;  // dense indices: the rebuild maps its node list back to ids
+          dst[p] = v;
+        }
       }
     }
+    __syncthreads();
   }
+}
+
+// node list of the rebuilt core: dense indices of the old graph -> ids
+__global__ void __launch_bounds__(256) kcore_ids_kernel(const int64_t* __restrict__ old_ids,
+                                                        int64_t n, int64_t* __restrict__ ids) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) ids[i] = old_ids[ids[i]];
 }
 
 }  // namespace gtd
@@ -464,13 +496,17 @@ static gt_graph* kcore(const gt_graph* g, int32_t k) {
     GT_CUDA(cudaMemsetAsync(ecount, 0, 8, s));
     {
       Phase ph("kcore.edges", 16.0 * g->e + 8.0 * n);
-      GT_LAUNCH(gtd::kcore_edges_kernel, warps_grid(n), 256, 0, g->ids, g->out_off, g->out_adj, n,
-                alive, src, dst, ecount);
+      GT_LAUNCH(gtd::kcore_edges_kernel,
+                static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div64(n, gtd::KC_ROWS),
+                                                                          8LL * ctx().sm_count))),
+                256, 0, g->ids, g->out_off, g->out_adj, n, alive, src, dst, ecount);
     }
     unsigned long long rows = 0;
     d2h(&rows, ecount, 8);
     sync();
     core = build_csr(src, dst, int64_t(rows), nullptr, 0, true);
+    if (core->n > 0)
+      GT_LAUNCH(gtd::kcore_ids_kernel, ceil_div(core->n, 256), 256, 0, g->ids, core->n, core->ids);
   } catch (...) {
     dfree(cat); dfree(deg); dfree(alive); dfree(q0); dfree(q1);
     if (src) dfree(src);
