@@ -198,3 +198,21 @@ def test_c5_shape_uniform_vs_oracle():
     assert got.shape == (1,)
     scores = np.asarray(pr.scores)
     assert np.abs(scores - ref.pagerank_csr(want, 0.85, 20)).sum() <= 1e-9
+
+
+@pytest.mark.slow
+def test_capacity_error_at_2_pow_31_nodes():
+    """>= 2^31 distinct ids do not fit the int32 dense adjacency: CapacityError.
+    The reference switches to searchsorted there (convert.py:55-59) and keeps
+    going on the host; this build states its limit instead of
+    overflowing the int32 indices."""
+    import torch
+
+    ids = torch.arange(1 << 31, dtype=torch.int64, device="cuda")
+    with pytest.raises(gt.CapacityError):
+        gt.table_to_graph(gt.edge_table(ids, ids), SPEC)
+    del ids
+    torch.cuda.empty_cache()
+    # the library stays usable afterwards
+    g = gt.table_to_graph(gt.edge_table(np.array([1, 2]), np.array([2, 1])), SPEC)
+    assert g.edge_count == 2
