@@ -584,10 +584,18 @@ def ours_arm(args):
         state.clear()
         torch.cuda.empty_cache()
 
+        pipe = {"next": None}
         if not sharded:
             def e2e_step():
+                # pipelined ingest: this step's table was copied (pinned host ->
+                # HBM, side stream) while the previous step computed; the next
+                # step's copy is issued now and overlaps this step's PageRank
+                # and triangle count
                 t0_ = time.perf_counter()
-                g = gt.table_to_graph(host_table, edge_spec)
+                cur = pipe["next"] if pipe["next"] is not None else host_table.prefetch()
+                g = gt.table_to_graph(cur, edge_spec)
+                del cur
+                pipe["next"] = host_table.prefetch()
                 t1_ = time.perf_counter()
                 pr = gt.pagerank(g, 0.85, iters)
                 t2_ = time.perf_counter()
@@ -621,6 +629,7 @@ def ours_arm(args):
             pr, tc2 = e2e_step()
         e1.record(stream)
         e1.synchronize()
+        torch.cuda.synchronize()  # the copy issued by the last step completes inside the region
         wall = time.perf_counter() - t0
         barrier()
         e2e_ms = max(e0.elapsed_time(e1), wall * 1e3) / args.steps
@@ -633,8 +642,13 @@ def ours_arm(args):
         assert tc2 == tc, "e2e triangle count differs from the device-resident run"
         e2e = {"value": rows * world / (e2e_ms / 1e3), "unit": "rows/s",
                "ms_per_step": e2e_ms, "h2d_bytes_per_step": 16 * rows,
+               "pipelined": (None if sharded else
+                             "ColumnTable.prefetch: each step's table is copied from pinned "
+                             "host memory on a side stream while the previous step computes; "
+                             "one copy per timed step, all inside the timed region"),
                "d2h_bytes_per_step": 16 * n + 8 + 8,
-               "api": "table_to_graph(host ColumnTable) -> pagerank"
+               "api": ("host ColumnTable.prefetch -> table_to_graph" if not sharded
+                       else "table_to_graph(host ColumnTable)") + " -> pagerank"
                       f"{' -> triangle_count' if with_tc else ''}"}
 
     cpu = None

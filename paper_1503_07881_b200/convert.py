@@ -68,6 +68,8 @@ def table_to_graph(table, spec: EdgeSpec, workers: int | None = None) -> DeviceG
     """
     spec.validate(table)
     resolve_workers(workers)
+    if hasattr(table, "_await_ready"):
+        table._await_ready()
     src = table.column(spec.src_col)
     dst = table.column(spec.dst_col)
     s_keep, s_ptr = _device_ptr(src)

@@ -147,6 +147,7 @@ def select(table: ColumnTable, pred: Predicate, in_place: bool = False) -> Colum
     """Rows satisfying pred, ids and order preserved; optionally in place
     (tables.py:325-344). The result is device-resident."""
     typ = _check_predicate(table, pred)
+    table._await_ready()
     torch = _torch()
     device = _device_of(table)
     n = table.n_rows
@@ -230,6 +231,8 @@ def join(left: ColumnTable, right: ColumnTable, left_col: str, right_col: str) -
     if lt != rt:
         raise TypeMismatchError(
             f"join columns {left_col!r} ({lt}) and {right_col!r} ({rt}) differ in type")
+    left._await_ready()
+    right._await_ready()
     torch = _torch()
     device = _device_of(left, right)
     schema = _suffixed_schema(left.schema, right.schema)

@@ -97,6 +97,7 @@ class ColumnTable:
         if row_ids is not None and _length(row_ids) != n:
             raise SchemaError("row_ids length does not match the columns")
         self._row_ids = row_ids
+        self._ready = None  # pending prefetch (event, device tensors)
         if next_row_id is None:
             next_row_id = n if row_ids is None else (int(row_ids.max()) + 1 if n else 0)
         self._next_row_id = int(next_row_id)
@@ -185,6 +186,56 @@ class ColumnTable:
         return ColumnTable(self.schema, cols, pool=self.pool, row_ids=ids,
                            next_row_id=self._next_row_id)
 
+    def prefetch(self, device=None) -> "ColumnTable":
+        """Device-resident copy of the table whose host→device transfer runs on
+        a side stream and returns at once. The library waits for the copy only
+        when a call first uses the table (``_await_ready``), so a copy issued
+        while the library is busy overlaps that work (pipelined ingest of a
+        stream of tables). Host columns should be pinned for the copy to be
+        asynchronous; str codes travel as int64, floats as float64."""
+        import torch
+
+        from . import _native
+
+        dev = torch.device("cuda", _native.device_ordinal()) if device is None \
+            else torch.device(device)
+        side = _copy_stream(dev)
+        cols = []
+        with torch.cuda.stream(side):
+            for (_, typ), col in zip(self.schema.columns, self.columns):
+                if _is_device(col):
+                    cols.append(col)
+                    continue
+                dt = np.float64 if typ == FLOAT else np.int64
+                t = col if isinstance(col, torch.Tensor) else \
+                    torch.from_numpy(np.ascontiguousarray(col, dtype=dt))
+                cols.append(t.to(dev, non_blocking=True))
+        ev = torch.cuda.Event()
+        ev.record(side)
+        out = ColumnTable(self.schema, cols, pool=self.pool, row_ids=None,
+                          next_row_id=self._next_row_id)
+        if self._row_ids is not None:
+            out._row_ids = self._row_ids
+        out._ready = (ev, [c for c in cols if c.device == dev])
+        return out
+
+    def _await_ready(self) -> None:
+        """Make the library stream wait for a pending prefetch of this table."""
+        ready = getattr(self, "_ready", None)
+        if ready is None:
+            return
+        import torch
+
+        from . import _native
+
+        ev, tensors = ready
+        dev = tensors[0].device if tensors else torch.device("cuda", _native.device_ordinal())
+        lib = torch.cuda.ExternalStream(_native.stream_handle(), device=dev)
+        lib.wait_event(ev)
+        for t in tensors:
+            t.record_stream(lib)
+        self._ready = None
+
     def to_host(self) -> "ColumnTable":
         cols = [c.cpu().numpy() if _is_device(c) else c for c in self.columns]
         ids = self._row_ids
@@ -211,6 +262,18 @@ class ColumnTable:
 
     def __repr__(self):
         return f"ColumnTable({self.schema!r}, rows={self.n_rows})"
+
+
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream(dev):
+    import torch
+
+    key = str(dev)
+    if key not in _COPY_STREAMS:
+        _COPY_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return _COPY_STREAMS[key]
 
 
 def load_tsv(path, schema: Schema, device=None) -> ColumnTable:
