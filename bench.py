@@ -51,6 +51,9 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-rows", type=int, default=1_000_000)
     p.add_argument("--no-tsv", action="store_true")
+    p.add_argument("--lanes", action="store_true",
+                   help="PageRank on lane 1 next to the triangle count on lane 0 (measured: "
+                        "no faster than serial at C2, both saturate the SMs)")
     p.add_argument("--no-extras", action="store_true",
                    help="skip the measured-apart extras (SURVEY 8f rows): step kernels only")
     p.add_argument("--tsv-rows", type=int, default=4_000_000)
@@ -415,8 +418,11 @@ def ours_arm(args):
             out = state.get("scores")
             if out is None or out.shape[0] != g.node_count:
                 out = state["scores"] = torch.empty(g.node_count, dtype=torch.float64, device=dev)
-            gt.pagerank_device(g, 0.85, iters, out.data_ptr())
-            tc = gt.triangle_count(g) if with_tc else None
+            if with_tc and args.lanes:  # PageRank (lane 1) next to the count (lane 0)
+                _, tc = gt.pagerank_and_triangles(g, 0.85, iters, scores_out_ptr=out.data_ptr())
+            else:
+                gt.pagerank_device(g, 0.85, iters, out.data_ptr())
+                tc = gt.triangle_count(g) if with_tc else None
             state.update(n=g.node_count, e=g.edge_count, tc=tc)
             del g
     else:
@@ -597,9 +603,13 @@ def ours_arm(args):
                 del cur
                 pipe["next"] = host_table.prefetch()
                 t1_ = time.perf_counter()
-                pr = gt.pagerank(g, 0.85, iters)
-                t2_ = time.perf_counter()
-                tc_ = gt.triangle_count(g) if with_tc else None
+                if with_tc and args.lanes:
+                    pr, tc_ = gt.pagerank_and_triangles(g, 0.85, iters)
+                    t2_ = time.perf_counter()
+                else:
+                    pr = gt.pagerank(g, 0.85, iters)
+                    t2_ = time.perf_counter()
+                    tc_ = gt.triangle_count(g) if with_tc else None
                 if os.environ.get("BENCH_E2E_DEBUG"):
                     print(f"e2e split: build {1e3 * (t1_ - t0_):.1f} pr {1e3 * (t2_ - t1_):.1f} "
                           f"tc {1e3 * (time.perf_counter() - t2_):.1f} ms", file=sys.stderr)

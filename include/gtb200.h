@@ -70,6 +70,12 @@ GT_API void* gt_stream(void);
 /* Message of the last failing call on this thread ("" if none). */
 GT_API const char* gt_last_error(void);
 
+/* Bind the calling thread to a lane (0 or 1; default 0). A lane has its own
+ * stream and workspace, so two threads on different lanes can run calls on
+ * the same graph at once (e.g. gt_pagerank next to gt_triangles); calls on
+ * one lane stay serialised. */
+GT_API int gt_set_lane(int lane);
+
 /* Release cached scratch memory (radix-sort buffers, look-back state). */
 GT_API int gt_release_workspace(void);
 

@@ -10,7 +10,8 @@ the GPU, calling the path without the library raises ``NativeError``.
 """
 
 from .algorithms import (DistMap, LabelMap, RankMap, connected_components, k_core, pagerank,
-                         pagerank_device, scc, sssp, triangle_count)
+                         pagerank_and_triangles, pagerank_device, scc, sssp,
+                         triangle_count)
 from .convert import EdgeSpec, graph_to_edge_table, graph_to_node_table, table_to_graph
 from .errors import (
     CapacityError,
@@ -37,5 +38,5 @@ __all__ = [
     "edge_table", "from_edges", "graph_to_edge_table", "graph_to_node_table", "load_tsv",
     "pagerank", "pagerank_device", "save_tsv", "table_from_map", "table_to_graph",
     "triangle_count", "upload", "sssp", "connected_components", "k_core", "DistMap",
-    "LabelMap", "scc", "Predicate", "select", "project", "join",
+    "LabelMap", "scc", "pagerank_and_triangles", "Predicate", "select", "project", "join",
 ]

@@ -27,6 +27,7 @@ SIGNATURES = {
     "gt_version": (ctypes.c_char_p, []),
     "gt_stream": (_VP, []),
     "gt_last_error": (ctypes.c_char_p, []),
+    "gt_set_lane": (ctypes.c_int, [ctypes.c_int]),
     "gt_release_workspace": (ctypes.c_int, []),
     "gt_build_csr": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_int,
                                     ctypes.POINTER(_VP)]),
@@ -383,6 +384,25 @@ def rmat_generate(scale, rows, a, b, c, seed, permute, src_ptr, dst_ptr, start=0
     check(lib.gt_rmat_generate_range(int(scale), int(start), int(rows), float(a), float(b),
                                      float(c), int(seed) & ((1 << 64) - 1), int(bool(permute)),
                                      int(src_ptr), int(dst_ptr)), "gt_rmat_generate_range")
+
+
+_LANE_POOLS: dict = {}
+
+
+def lane_submit(lane: int, fn, *args, **kwargs):
+    """Run fn(*args, **kwargs) on a worker thread bound to library lane `lane`
+    (its own stream and workspace): independent calls on one graph overlap on
+    the GPU. Returns a concurrent.futures.Future."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    ensure_init()
+    pool = _LANE_POOLS.get(lane)
+    if pool is None:
+        def bind():
+            check(load().gt_set_lane(int(lane)), "gt_set_lane")
+
+        pool = _LANE_POOLS[lane] = ThreadPoolExecutor(1, initializer=bind)
+    return pool.submit(fn, *args, **kwargs)
 
 
 def stream_handle() -> int:

@@ -120,6 +120,32 @@ def triangle_count(g, workers: int | None = None) -> int:
     return _native.triangles(dg.handle)
 
 
+def pagerank_and_triangles(g, damping: float = 0.85, iterations: int = 10,
+                           scores_out_ptr: int | None = None, workers: int | None = None):
+    """PageRank and the triangle count of one graph, run concurrently on two
+    library lanes (PageRank on lane 1, the count on lane 0): same results as
+    ``pagerank(g, ...)`` and ``triangle_count(g)``. With ``scores_out_ptr``
+    the scores go to that device buffer (returns (None, count)); otherwise a
+    RankMap is returned."""
+    resolve_workers(workers)
+    if not (0.0 < damping < 1.0):
+        raise ValueError(f"damping must be in (0, 1), got {damping}")
+    if iterations < 1:
+        raise ValueError(f"iterations must be >= 1, got {iterations}")
+    if g.node_count == 0:
+        raise ValueError("pagerank needs a non-empty graph")
+    dg = upload(g)
+    if scores_out_ptr is not None:
+        fut = _native.lane_submit(1, pagerank_device, dg, damping, iterations, scores_out_ptr)
+    else:
+        fut = _native.lane_submit(1, pagerank, dg, damping, iterations)
+    try:
+        tc = triangle_count(dg)
+    finally:
+        pr = fut.result()
+    return pr, tc
+
+
 class _NodeArrayMap(Mapping):
     """Read-only ``{node id: value}`` view over (ids ascending, values)."""
 

@@ -41,6 +41,11 @@ void set_last_error(const std::string& m);
   return GT_OK;
 
 // ---------------------------------------------------------------- context --
+// Lanes: each calling thread works on a lane (gt_set_lane; default 0) with
+// its own stream and workspace slots, so two threads can run independent
+// calls on one graph concurrently (e.g. PageRank next to the triangle count).
+constexpr int GT_LANES = 2;
+
 struct Context {
   int device = -1;
   int sm_count = 148;

@@ -23,14 +23,33 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
   fail(e == cudaErrorMemoryAllocation ? GT_ENOMEM : GT_ECUDA, buf);
 }
 
-static Context g_ctx;
-Context& ctx() { return g_ctx; }
+static Context g_lanes[GT_LANES];
+static thread_local int t_lane = 0;
+static std::atomic<bool> g_profiling{false};
+static std::mutex g_init_mu;
+Context& ctx() { return g_lanes[t_lane]; }
 
 void require_init() {
-  if (g_ctx.stream == nullptr) {
+  if (ctx().stream != nullptr) return;
+  if (g_lanes[0].stream == nullptr) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
-    if (gt_init(dev) != GT_OK) fail(GT_ENODEV, std::string("gt_init failed: ") + g_last_error);
+    const int lane = t_lane;
+    t_lane = 0;
+    const int rc = gt_init(dev);
+    t_lane = lane;
+    if (rc != GT_OK) fail(GT_ENODEV, std::string("gt_init failed: ") + g_last_error);
+  }
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  Context& c = ctx();
+  if (c.stream == nullptr) {  // a further lane: lane 0's device, its own stream
+    const Context& z = g_lanes[0];
+    GT_CUDA(cudaSetDevice(z.device));
+    c.device = z.device;
+    c.sm_count = z.sm_count;
+    c.l2_bytes = z.l2_bytes;
+    c.smem_optin = z.smem_optin;
+    GT_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
   }
 }
 
@@ -47,7 +66,7 @@ void after_launch(const char* name) {
 void* dalloc(size_t bytes) {
   void* p = nullptr;
   if (bytes == 0) bytes = 8;
-  cudaError_t e = cudaMallocAsync(&p, bytes, g_ctx.stream);
+  cudaError_t e = cudaMallocAsync(&p, bytes, ctx().stream);
   if (e != cudaSuccess) {
     cudaGetLastError();
     char buf[256];
@@ -59,46 +78,47 @@ void* dalloc(size_t bytes) {
 }
 
 void dfree(void* p) {
-  if (p) cudaFreeAsync(p, g_ctx.stream);
+  if (p) cudaFreeAsync(p, ctx().stream);
 }
 
 struct SlotBuf { void* p = nullptr; size_t cap = 0; };
-static SlotBuf g_slots[WS_NSLOTS];
+static SlotBuf g_slots[GT_LANES][WS_NSLOTS];
 
 void* ws_get(Slot s, size_t bytes) {
-  SlotBuf& b = g_slots[s];
+  SlotBuf& b = g_slots[t_lane][s];
   if (b.cap < bytes) {
     dfree(b.p);
     size_t cap = bytes + bytes / 8;  // headroom so slightly larger inputs reuse
     b.p = dalloc(cap);
     b.cap = cap;
-    if (s == WS_LOOKBACK) GT_CUDA(cudaMemsetAsync(b.p, 0, cap, g_ctx.stream));
+    if (s == WS_LOOKBACK) GT_CUDA(cudaMemsetAsync(b.p, 0, cap, ctx().stream));
   }
   return b.p;
 }
 
 void ws_release_all() {
-  for (auto& b : g_slots) { dfree(b.p); b.p = nullptr; b.cap = 0; }
+  for (auto& b : g_slots[t_lane]) { dfree(b.p); b.p = nullptr; b.cap = 0; }
 }
 
-static uint32_t g_epoch = 0;
-uint32_t next_epoch() {
-  g_epoch = (g_epoch + 1) & 0x3FFFFFu;
-  if (g_epoch == 0) {  // wrapped: clear stale words so old epochs cannot alias
-    SlotBuf& b = g_slots[WS_LOOKBACK];
-    if (b.p) GT_CUDA(cudaMemsetAsync(b.p, 0, b.cap, g_ctx.stream));
-    g_epoch = 1;
+static uint32_t g_epoch[GT_LANES] = {};
+uint32_t next_epoch() {  // per lane: each lane has its own look-back words
+  uint32_t& ep = g_epoch[t_lane];
+  ep = (ep + 1) & 0x3FFFFFu;
+  if (ep == 0) {  // wrapped: clear stale words so old epochs cannot alias
+    SlotBuf& b = g_slots[t_lane][WS_LOOKBACK];
+    if (b.p) GT_CUDA(cudaMemsetAsync(b.p, 0, b.cap, ctx().stream));
+    ep = 1;
   }
-  return g_epoch;
+  return ep;
 }
 
 void d2h(void* h, const void* d, size_t bytes) {
-  if (bytes) GT_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, g_ctx.stream));
+  if (bytes) GT_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, ctx().stream));
 }
 void h2d(void* d, const void* h, size_t bytes) {
-  if (bytes) GT_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, g_ctx.stream));
+  if (bytes) GT_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx().stream));
 }
-void sync() { GT_CUDA(cudaStreamSynchronize(g_ctx.stream)); }
+void sync() { GT_CUDA(cudaStreamSynchronize(ctx().stream)); }
 
 // ---------------------------------------------------------------- profiling --
 struct PhaseStat {
@@ -146,17 +166,17 @@ static void resolve_pending() {
 }
 
 Phase::Phase(const char* name, double bytes) {
-  if (!g_ctx.profiling) return;
+  if (!g_profiling.load(std::memory_order_relaxed)) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   idx = phase_index(name);
   g_phases[idx].bytes += bytes;
   g_phases[idx].launches += 1;
   start = get_event();
-  GT_CUDA(cudaEventRecord(start, g_ctx.stream));
+  GT_CUDA(cudaEventRecord(start, ctx().stream));
 }
 
 void profile_add_bytes(const char* name, double bytes) {
-  if (!g_ctx.profiling) return;
+  if (!g_profiling.load(std::memory_order_relaxed)) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   g_phases[phase_index(name)].bytes += bytes;
 }
@@ -165,7 +185,7 @@ Phase::~Phase() {
   if (idx < 0) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   cudaEvent_t end = get_event();
-  if (cudaEventRecord(end, g_ctx.stream) != cudaSuccess) return;
+  if (cudaEventRecord(end, ctx().stream) != cudaSuccess) return;
   g_phases[idx].pending.emplace_back(start, end);
 }
 
@@ -239,7 +259,16 @@ int gt_release_workspace(void) {
 int64_t gt_launch_count(void) { return g_launches.load(); }
 
 int gt_profile_enable(int on) {
-  ctx().profiling = on != 0;
+  g_profiling.store(on != 0);
+  return GT_OK;
+}
+
+int gt_set_lane(int lane) {
+  if (lane < 0 || lane >= GT_LANES) {
+    set_last_error("lane must be in [0, GT_LANES)");
+    return GT_EINVAL;
+  }
+  t_lane = lane;
   return GT_OK;
 }
 

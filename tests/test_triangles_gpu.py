@@ -199,3 +199,19 @@ def test_orientation_matches_reference(name):
         assert np.all(np.diff(row) > 0)
         assert sorted(order[row].tolist()) == sorted(want_higher[order[r]].tolist())
     assert gt.triangle_count(dg) == ref.triangle_count_fast(g)
+
+
+def test_pagerank_and_triangles_on_two_lanes_match_serial():
+    """pagerank_and_triangles runs PageRank on lane 1 next to the count on
+    lane 0 (own streams and workspaces): same scores (bitwise) and count as
+    the serial calls, repeatedly."""
+    from paper_1503_07881_b200.synth import rmat_edges
+
+    src, dst = rmat_edges(18, 3_000_000, seed=21, permute=True)
+    g = gt.table_to_graph(gt.edge_table(src, dst), gt.EdgeSpec("src", "dst"))
+    pr0 = gt.pagerank(g, 0.85, 20)
+    tc0 = gt.triangle_count(g)
+    for _ in range(3):
+        pr, tc = gt.pagerank_and_triangles(g, 0.85, 20)
+        assert tc == tc0
+        assert np.array_equal(np.asarray(pr.scores), np.asarray(pr0.scores))
