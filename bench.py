@@ -601,15 +601,29 @@ def ours_arm(args):
                 cur = pipe["next"] if pipe["next"] is not None else host_table.prefetch()
                 g = gt.table_to_graph(cur, edge_spec)
                 del cur
-                pipe["next"] = host_table.prefetch()
+                if not os.environ.get("BENCH_E2E_SERIAL"):
+                    pipe["next"] = host_table.prefetch()
                 t1_ = time.perf_counter()
+                # scores stay in HBM until the count is done, then one D2H read:
+                # a read issued while the next table's H2D copy is in flight
+                # waited for that copy (C4: +410 ms), one after the count does not
+                n_ = g.node_count
+                d_sc = pipe.get("d_sc")
+                if d_sc is None or d_sc.shape[0] < n_:
+                    d_sc = pipe["d_sc"] = torch.empty(n_, dtype=torch.float64, device=dev)
+                    pipe["h_sc"] = [torch.empty(n_, dtype=torch.float64, pin_memory=True)
+                                    for _ in range(2)]
                 if with_tc and args.lanes:
-                    pr, tc_ = gt.pagerank_and_triangles(g, 0.85, iters)
+                    _, tc_ = gt.pagerank_and_triangles(g, 0.85, iters,
+                                                       scores_out_ptr=d_sc.data_ptr())
                     t2_ = time.perf_counter()
                 else:
-                    pr = gt.pagerank(g, 0.85, iters)
+                    gt.pagerank_device(g, 0.85, iters, d_sc.data_ptr())
                     t2_ = time.perf_counter()
                     tc_ = gt.triangle_count(g) if with_tc else None
+                pipe["flip"] = 1 - pipe.get("flip", 0)
+                pr = pipe["h_sc"][pipe["flip"]][:n_]
+                pr.copy_(d_sc[:n_])  # device -> pinned host, synchronous
                 if os.environ.get("BENCH_E2E_DEBUG"):
                     print(f"e2e split: build {1e3 * (t1_ - t0_):.1f} pr {1e3 * (t2_ - t1_):.1f} "
                           f"tc {1e3 * (time.perf_counter() - t2_):.1f} ms", file=sys.stderr)
@@ -656,10 +670,11 @@ def ours_arm(args):
                              "ColumnTable.prefetch: each step's table is copied from pinned "
                              "host memory on a side stream while the previous step computes; "
                              "one copy per timed step, all inside the timed region"),
-               "d2h_bytes_per_step": 16 * n + 8 + 8,
-               "api": ("host ColumnTable.prefetch -> table_to_graph" if not sharded
-                       else "table_to_graph(host ColumnTable)") + " -> pagerank"
-                      f"{' -> triangle_count' if with_tc else ''}"}
+               "d2h_bytes_per_step": (8 * n + 8) if not sharded else 16 * n + 8 + 8,
+               "api": (("host ColumnTable.prefetch -> table_to_graph -> pagerank_device"
+                        if not sharded else "table_to_graph(host ColumnTable) -> pagerank")
+                       + (" -> triangle_count" if with_tc else "")
+                       + (" -> scores to pinned host" if not sharded else ""))}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -33,6 +33,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 namespace gtd {
 
@@ -47,6 +48,18 @@ __device__ __forceinline__ double pr_gather(const double* contrib, int32_t u) {
   if (u < PR_HOT) return __ldg(contrib + u);
   double v;
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(contrib + u));
+  return v;
+}
+
+// Same, with an L2 cache policy on the tail loads (createpolicy.range: the
+// hot head of contrib evict_last, the rest evict_first) — L2 residency for
+// the hot sources without a persisting set-aside, whose set-up and release
+// (cudaDeviceSetLimit, cudaCtxResetPersistingL2Cache) synchronise the device.
+__device__ __forceinline__ double pr_gather_pol(const double* contrib, int32_t u, uint64_t pol) {
+  if (u < PR_HOT) return __ldg(contrib + u);
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(contrib + u), "l"(pol));
   return v;
 }
 
@@ -255,7 +268,7 @@ __device__ __forceinline__ void pr_tile(
     const double* __restrict__ inv_out, const int32_t* __restrict__ pos, double base,
     double damping, double* __restrict__ score, double* __restrict__ contrib_next,
     double* __restrict__ head, double* __restrict__ tail, int64_t* __restrict__ tail_row,
-    double* __restrict__ dpart, bool last) {
+    double* __restrict__ dpart, bool last, uint32_t hot_bytes, uint32_t total_bytes) {
   const int64_t e0 = c * PR_TILE;
   const int64_t e1 = min(e, e0 + PR_TILE);
   const int ne = e1 > e0 ? int(e1 - e0) : 0;
@@ -287,10 +300,21 @@ __device__ __forceinline__ void pr_tile(
       sr.pos[r] = pos ? pos[row] : int32_t(row);
     }
   }
+  if (hot_bytes) {
+    uint64_t pol;
+    asm volatile("createpolicy.range.global.L2::evict_last.L2::evict_first.b64 %0, [%1], %2, %3;"
+                 : "=l"(pol) : "l"(contrib), "r"(hot_bytes), "r"(total_bytes));
 #pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    const int j = i * PR_THREADS + ltid;
-    if (j < ne) vals[j] = pr_gather(contrib, idx[i]);
+    for (int i = 0; i < PER; ++i) {
+      const int j = i * PR_THREADS + ltid;
+      if (j < ne) vals[j] = pr_gather_pol(contrib, idx[i], pol);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int j = i * PR_THREADS + ltid;
+      if (j < ne) vals[j] = pr_gather(contrib, idx[i]);
+    }
   }
   bar();
 
@@ -310,14 +334,14 @@ __global__ void __launch_bounds__(PR_THREADS, PR_MIN_BLOCKS) pr_spmv_kernel(
     const double* __restrict__ dangling_prev, double damping,
     double* __restrict__ score, double* __restrict__ contrib_next, double* __restrict__ head,
     double* __restrict__ tail, int64_t* __restrict__ tail_row, double* __restrict__ dpart,
-    int last_iter) {
+    int last_iter, uint32_t hot_bytes, uint32_t total_bytes) {
   __shared__ double vals[PR_TILE];
   __shared__ PrRows sr;
   const double base =
       (1.0 - damping) / double(n_total) + damping * (*dangling_prev / double(n_total));
   pr_tile(int64_t(blockIdx.x), int(threadIdx.x), [] { __syncthreads(); }, vals, sr, in_off,
           in_adj, n, e, tile_row, contrib, inv_out, pos, base, damping, score, contrib_next, head,
-          tail, tail_row, dpart, last_iter != 0);
+          tail, tail_row, dpart, last_iter != 0, hot_bytes, total_bytes);
 }
 
 __global__ void __launch_bounds__(256) pr_fixup_kernel(
@@ -463,7 +487,21 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
   // marks its hot head as persisting for the gathers of each iteration.
   const size_t contrib_bytes = size_t(n) * 8;
   size_t window = 0;
-  if (contrib_bytes > ctx().l2_bytes / 2 && !getenv("GT_PR_NO_L2_WINDOW")) {
+  uint32_t hot_bytes = 0, total_bytes = 0;
+  static int l2_mode = -1;  // GT_PR_L2: "policy" (default), "window" (set-aside), "none"
+  if (l2_mode < 0) {
+    const char* v = getenv("GT_PR_L2");
+    l2_mode = (v && !strcmp(v, "window")) ? 1 : (v && !strcmp(v, "none")) ? 2 : 0;
+  }
+  if (contrib_bytes > ctx().l2_bytes / 2 && l2_mode == 0 && contrib_bytes < (size_t(1) << 32)) {
+    int max_win = 0;
+    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, ctx().device);
+    int persist_max = 0;
+    cudaDeviceGetAttribute(&persist_max, cudaDevAttrMaxPersistingL2CacheSize, ctx().device);
+    hot_bytes = uint32_t(std::min<size_t>({contrib_bytes, size_t(max_win), size_t(persist_max)}));
+    total_bytes = uint32_t(contrib_bytes);
+  }
+  if (contrib_bytes > ctx().l2_bytes / 2 && l2_mode == 1) {
     int max_win = 0;
     cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, ctx().device);
     int persist_max = 0;
@@ -490,7 +528,7 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
       Phase ph("pr.spmv", 12.0 * e + 8.0 * (n + 1) + 20.0 * n);
       GT_LAUNCH(gtd::pr_spmv_kernel, static_cast<int>(tiles), gtd::PR_THREADS, 0, g->in_off,
                 in_adj_r, n, e, n, tile_row, cur, inv_out, pos, dang + it, damping, score, nxt,
-                head, tail, tail_row, dpart, last);
+                head, tail, tail_row, dpart, last, hot_bytes, total_bytes);
     }
     {
       Phase ph("pr.fixup", 40.0 * tiles);
@@ -557,7 +595,7 @@ static void pr_step_impl(const int64_t* in_off, const int32_t* in_adj, int64_t r
             tile_row);
   GT_LAUNCH(gtd::pr_spmv_kernel, static_cast<int>(tiles), gtd::PR_THREADS, 0, in_off, in_adj, rows,
             e, n_total, tile_row, contrib_full, inv_rows, (const int32_t*)nullptr, dangling_prev,
-            damping, score_rows, contrib_rows, head, tail, tail_row, dpart, last);
+            damping, score_rows, contrib_rows, head, tail, tail_row, dpart, last, 0u, 0u);
   GT_LAUNCH(gtd::pr_fixup_kernel, fix_blocks, 256, 0, in_off, rows, n_total, tiles, inv_rows,
             (const int32_t*)nullptr, dangling_prev, damping, head, tail, tail_row, dpart,
             score_rows, contrib_rows, last, partials, ticket, dangling_out);
