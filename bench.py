@@ -509,7 +509,9 @@ def ours_arm(args):
     dom_gbs = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
     roofline = {"bound": "hbm", "kernel": dom_name,
                 "achieved": dom_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": dom_gbs / pk["hbm_gbs"], "traffic": ncu_traffic(args.config, dom_name),
+                "frac": dom_gbs / pk["hbm_gbs"],
+                "traffic": (ncu_traffic(args.config, dom_name) or {}).get("bytes_per_launch"),
+                "traffic_source": ncu_traffic(args.config, dom_name),
                 "bytes_per_launch": dom_bytes / max(dom_cnt, 1),
                 "ms_per_launch": dom_ms / max(dom_cnt, 1), "peak_source": pk["source"],
                 "share_of_step": dom_ms / elapsed_ms}
