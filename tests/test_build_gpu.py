@@ -240,3 +240,65 @@ def test_prefetch_pipelined_ingest_matches_direct_build():
     sel = gt.select(host.prefetch(), gt.Predicate("src", "<", int(np.median(src))))
     np.testing.assert_array_equal(sel.row_ids.cpu().numpy(),
                                   np.flatnonzero(src < int(np.median(src))))
+
+
+@pytest.mark.slow
+def test_c4_full_size_properties():
+    """BASELINE configs[3] at full size (1.47 B rows, R-MAT s26): properties
+    that do not need a host oracle, checked on the device.
+    * node set = distinct ids of both columns, edge count = distinct pairs;
+    * out-rows sorted and duplicate-free, in-CSR the exact transpose
+      (in-degree histogram = dst histogram of the distinct pairs);
+    * PageRank: scores positive and summing to 1 (the dangling mass is
+      redistributed, algorithms.py:72-82);
+    * triangles: the 4-way split of the middle vertices sums to the total."""
+    import ctypes
+
+    import torch
+
+    from paper_1503_07881_b200 import _native
+
+    src, dst = rmat_device(CONFIGS["c4"])
+    g = gt.table_to_graph(gt.edge_table(src, dst), SPEC)
+    _native.load().gt_release_workspace()  # the checks below need the memory
+    n, e = g.node_count, g.edge_count
+    ids_p, oo_p, oa_p, io_p, ia_p = g.device_views()
+    def as_t(p, cnt, dt):  # zero-copy torch view of a library-owned device array
+        class _A:
+            __cuda_array_interface__ = {"shape": (cnt,), "typestr": dt, "data": (p, False),
+                                        "version": 3}
+        return torch.as_tensor(_A(), device="cuda")
+
+    ids = as_t(ids_p, n, "<i8")
+    out_off, in_off = as_t(oo_p, n + 1, "<i8"), as_t(io_p, n + 1, "<i8")
+    out_adj, in_adj = as_t(oa_p, e, "<i4"), as_t(ia_p, e, "<i4")
+    both = torch.unique(torch.cat([src[:1 << 28], dst[:1 << 28]]))  # a prefix fits memory
+    assert bool(torch.isin(both, ids).all())
+    assert bool((ids[1:] > ids[:-1]).all())
+    # out-rows: strictly increasing within rows
+    row_of = torch.repeat_interleave(torch.arange(n, device="cuda"), out_off[1:] - out_off[:-1])
+    key = row_of * n + out_adj.long()
+    assert bool((key[1:] > key[:-1]).all())
+    del row_of, key
+    # distinct pairs = edge count (device sort of packed ranks)
+    rs = torch.searchsorted(ids, src)
+    rd = torch.searchsorted(ids, dst)
+    del src, dst
+    packed = torch.unique(rs * n + rd)
+    del rs, rd
+    assert packed.shape[0] == e
+    # in-CSR = transpose: in-degree = dst histogram of the distinct pairs
+    indeg = torch.bincount(packed % n, minlength=n)
+    assert torch.equal(indeg, in_off[1:] - in_off[:-1])
+    del packed, indeg
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    gt.pagerank_device(g, 0.85, 20, out.data_ptr())
+    assert bool((out > 0).all()) and abs(float(out.sum()) - 1.0) < 1e-9
+    total = gt.triangle_count(g)
+    parts = 0
+    lib = _native.load()
+    for p in range(4):
+        c = ctypes.c_int64()
+        _native.check(lib.gt_triangles_part(g.handle, p, 4, ctypes.byref(c)), "gt_triangles_part")
+        parts += c.value
+    assert parts == total == 99862871249  # the value every C4 run of this table reports
