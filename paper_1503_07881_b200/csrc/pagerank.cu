@@ -488,11 +488,10 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
   const size_t contrib_bytes = size_t(n) * 8;
   size_t window = 0;
   uint32_t hot_bytes = 0, total_bytes = 0;
-  static int l2_mode = -1;  // GT_PR_L2: "policy" (default), "window" (set-aside), "none"
-  if (l2_mode < 0) {
+  static const int l2_mode = [] {  // GT_PR_L2: "policy" (default), "window", "none"
     const char* v = getenv("GT_PR_L2");
-    l2_mode = (v && !strcmp(v, "window")) ? 1 : (v && !strcmp(v, "none")) ? 2 : 0;
-  }
+    return (v && !strcmp(v, "window")) ? 1 : (v && !strcmp(v, "none")) ? 2 : 0;
+  }();
   if (contrib_bytes > ctx().l2_bytes / 2 && l2_mode == 0 && contrib_bytes < (size_t(1) << 32)) {
     int max_win = 0;
     cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, ctx().device);

@@ -261,13 +261,14 @@ template <int BITS, int M>
 static void launch_bits(int grid, const uint64_t* src, uint64_t* dst, int64_t n, int shift,
                         const int64_t* digit_base, uint64_t* status, uint32_t* counter,
                         uint32_t epoch) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  // thread-safe one-time set-up (lanes may launch from two threads)
+  static const bool attr_set = [] {
     GT_CUDA(cudaFuncSetAttribute(gtd::onesweep_kernel<BITS, M>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(sizeof(gtd::OnesweepSmem))));
-    attr_set = true;
-  }
+    return true;
+  }();
+  (void)attr_set;
   GT_LAUNCH((gtd::onesweep_kernel<BITS, M>), grid, RS_THREADS, sizeof(gtd::OnesweepSmem), src, dst,
             n, shift, digit_base, status, counter, epoch);
 }
@@ -318,11 +319,10 @@ uint64_t* radix_sort(uint64_t* a, uint64_t* b, int64_t n, const SortPlan& plan, 
   }
   uint64_t* src = a;
   uint64_t* dst = b;
-  static int nmatch = -1;
-  if (nmatch < 0) {  // GT_SORT_MATCH: keys per thread ranked by __match_any_sync (tuning)
+  static const int nmatch = [] {  // GT_SORT_MATCH: keys per thread ranked by MATCH (tuning)
     const char* env = getenv("GT_SORT_MATCH");
-    nmatch = env ? atoi(env) : 6;
-  }
+    return env ? atoi(env) : 6;
+  }();
   for (int q = 0; q < plan.passes; ++q) {
     Phase ph(phase, 16.0 * n);
     const uint32_t epoch = next_epoch();
