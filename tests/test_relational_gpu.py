@@ -196,3 +196,47 @@ def test_demo_chain_matches_reference():
     assert np.abs(got - qa["pr"]).sum() <= 1e-9
     with pytest.raises(graphdesk.FrontendError):
         graphdesk.Select(posts, "NoSuchColumn=1")
+
+
+# ------------------------------------------------------------ property-based --
+
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+_ROWS = st.lists(st.tuples(st.integers(-5, 5), st.sampled_from([0.0, -0.0, 1.5, float("nan")]),
+                           st.sampled_from(["a", "b", "", "zz"]), st.integers(-(2 ** 63), 2 ** 63 - 1)),
+                 max_size=60)
+
+
+@settings(max_examples=40, deadline=None)
+@given(_ROWS, _ROWS, st.sampled_from(["k", "x", "s", "v"]))
+def test_join_property_vs_oracle(lrows, rrows, key):
+    """Random tables (duplicates, +-0.0, NaN, int64 extremes, shared and
+    disjoint string pools): the device join equals the oracle's hash join
+    row for row, in order (tables.py:397-426)."""
+    left = make(list(SCHEMA.columns), lrows)
+    right = make(list(SCHEMA.columns), rrows)
+    got = gt.join(left, right, key, key)
+    i = "kxsv".index(key)
+
+    def keys(rows):  # as the reference hashes them: decoded, then .tolist() (fresh NaNs)
+        vals = [r[i] for r in rows]
+        return np.asarray(vals, dtype=np.float64).tolist() if key == "x" else vals
+
+    li, ri = ref.join_indices(keys(lrows), keys(rrows))
+    want = [lrows[a] + rrows[b] for a, b in zip(li.tolist(), ri.tolist())]
+    assert [tuple(map(repr, r)) for r in got.to_rows()] == [tuple(map(repr, r)) for r in want]
+
+
+@settings(max_examples=40, deadline=None)
+@given(_ROWS, st.sampled_from(["=", "!=", "<", "<=", ">", ">="]),
+       st.one_of(st.integers(-7, 7), st.floats(allow_nan=True, allow_infinity=True),
+                 st.integers(-(2 ** 70), 2 ** 70)))
+def test_select_int_property_vs_oracle(rows, op, value):
+    """INT column against ints, floats (non-integral, inf, NaN) and
+    beyond-int64 constants: numpy's comparison result (tables.py:343)."""
+    t = make(list(SCHEMA.columns), rows)
+    got = gt.select(t, gt.Predicate("v", op, value))
+    col = np.asarray([r[3] for r in rows], dtype=np.int64)
+    want = ref.select_indices(col, "int", [], op, value)
+    np.testing.assert_array_equal(host(got.row_ids), want)
