@@ -337,15 +337,20 @@ def build_csr(src: torch.Tensor, dst: torch.Tensor, group=None, ops=None) -> Sha
     o_lo, o_hi = out_bounds[rank], out_bounds[rank + 1]
     out_off, out_adj = ops.csr_from_keys(mine, kbits, o_lo, o_hi - o_lo)
 
-    # in-CSR: the owned edges as (dst, src), shuffled by dst range
-    ikeys = ops.sort_keys(ops.swap_halves(mine, kbits), 0, 2 * kbits)
+    # in-CSR: the owned edges as (dst, src), shuffled by dst range. `mine` is
+    # sorted by (src, dst), so after the swap a stable sort over the dst bits
+    # alone leaves src ascending inside every dst (the single-GPU in-sort)
+    ikeys = ops.sort_keys(ops.swap_halves(mine, kbits), kbits, 2 * kbits)
     del mine
     counts = ops.bucket_counts(ikeys, 2 * kbits - sb, 1 << sb)
     dist.all_reduce(counts, group=group)
     in_bounds = _range_bounds(counts.cpu().numpy(), world, n, bucket_rows)
     theirs = _shuffle_by_rows(ikeys, kbits, in_bounds, ops, group)
     del ikeys
-    theirs = ops.sort_keys(theirs, 0, 2 * kbits)
+    # the received runs arrive in source-rank order, each sorted by (dst, src),
+    # and rank r's sources all lie below rank r+1's (out-CSR ranges): a stable
+    # sort over the dst bits alone gives (dst, src) order
+    theirs = ops.sort_keys(theirs, kbits, 2 * kbits)
     i_lo, i_hi = in_bounds[rank], in_bounds[rank + 1]
     in_off, in_adj = ops.csr_from_keys(theirs, kbits, i_lo, i_hi - i_lo)
 
