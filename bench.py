@@ -1,21 +1,31 @@
 #!/usr/bin/env python
 """Benchmark of the hot path: ToGraph -> PageRank x20 -> triangle count.
 
-One "step" = one pass of the path over one R-MAT table (BASELINE.json
-configs[1] C2 by default: scale 22, 69M int64 rows, seed 2, permuted ids;
-triangles on its symmetrised version = configs[2] C3):
+One "step" = one pass of the path over one synthetic edge table, by default
+BASELINE.json configs[3] = C4 (R-MAT scale 26, 1.47 B int64 rows, seed 3,
+permuted ids; the north-star config), triangles on its symmetrised version:
     table_to_graph  ->  pagerank(d=0.85, 20 iterations, fp64)  ->  triangle_count
+`--config c2` runs configs[1] (69 M rows, + configs[2] triangles), `c5` the
+uniform 2.0 B-row contrast graph (ToGraph + PageRank only).
+
 `value` = input rows per second through the whole step (table already in
 HBM); `e2e` = the same through the public Python API with host (pinned)
 columns, host->device copy and result readback inside the timed region;
 `phases` break the step into the three rows of the metric, each in its own
 unit (build rows/s, PageRank edge-iterations/s, triangles undirected edges/s);
-`roofline` is the dominant kernel's algorithmic bytes / measured time vs the
-measured HBM copy peak (MEASURED_PEAKS.json).
+`roofline` = HBM roofline of the north-star kernels (build, PageRank) against
+the measured copy peak (MEASURED_PEAKS.json); the triangle count is issue-
+bound and reported as informational only.
 
-`--impl reference` times the reference's own CPU algorithm (the numpy
-restatement in oracle/, the reference being pure Python that is not shipped
-to the GPU box) on a bounded prefix sample of the same table.
+`--gpus N` runs N ranks (one process per GPU, NCCL): re-executed under
+torchrun when WORLD_SIZE is unset. Strong scaling: rank r generates rows
+[rR/N, (r+1)R/N) of the config's own table, the sharded pipeline
+(distributed.py) builds, ranks and counts it, and `value` = R / step time
+(max over ranks).
+
+`--impl reference` times the reference's own implementation (the unmodified
+`graphtables` package installed in baseline/_ref, all host cores) on a
+bounded same-family sample of the workload (see `reference_sample`).
 """
 
 from __future__ import annotations
@@ -45,11 +55,13 @@ def parse_args():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", choices=["c1", "c2", "c4", "c5"], default="c2")
+    p.add_argument("--config", choices=["c1", "c2", "c4", "c5"], default="c4")
     p.add_argument("--iterations", type=int, default=20)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-sample-rows", type=int, default=1_000_000)
+    p.add_argument("--cpu-sample-scale", type=int, default=14,
+                   help="R-MAT scale of the reference-arm / cpu_baseline sample (same a/b/c, "
+                        "edge factor and id permutation as the config)")
     p.add_argument("--no-tsv", action="store_true")
     p.add_argument("--lanes", action="store_true",
                    help="PageRank on lane 1 next to the triangle count on lane 0 (measured: "
@@ -60,6 +72,37 @@ def parse_args():
     p.add_argument("--sharded", action="store_true",
                    help="use the multi-GPU (distributed.py) pipeline even on one GPU")
     return p.parse_args()
+
+
+def shard_range(rank: int, world: int, rows: int):
+    """Rows [lo, hi) of the config's table that rank `rank` of `world` holds
+    (strong scaling: the ranks split one table)."""
+    return rows * rank // world, rows * (rank + 1) // world
+
+
+def torchrun_argv(gpus: int, argv, port: int):
+    """The re-exec command line for `--gpus N` without torchrun."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={gpus}", "--master-addr", "127.0.0.1",
+            "--master-port", str(port), str(Path(__file__).resolve()), *argv]
+
+
+def maybe_reexec(args):
+    """`--gpus N > 1` launched as a plain process: re-exec under torchrun (one
+    rank per GPU); fail loudly when fewer GPUs are visible."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return
+    import socket
+
+    import torch
+
+    visible = torch.cuda.device_count()
+    if visible < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but only {visible} CUDA device(s) visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.execv(sys.executable, torchrun_argv(args.gpus, sys.argv[1:], port))
 
 
 def peaks():
@@ -101,27 +144,86 @@ def spec_desc(name, spec, rows):
 
     if isinstance(spec, UniformSpec):
         return (f"{name}: uniform iid (Erdos-Renyi) {rows} rows over {spec.n_nodes} ids "
-                f"seed {spec.seed}")
-    return f"{name}: R-MAT s{spec.scale} {rows} rows seed {spec.seed} permuted={spec.permute}"
+                f"seed {spec.seed} (counter-based stand-in for synth.random_edges)")
+    perm = (f"ids Feistel-permuted over [0, 2^{spec.scale}) (stand-in for the dense "
+            f"remap)" if spec.permute else "ids unpermuted")
+    return f"{name}: R-MAT s{spec.scale} {rows} rows a/b/c={spec.a}/{spec.b}/{spec.c} " \
+           f"seed {spec.seed}, {perm}"
+
+
+def workload_desc(config, spec, iterations):
+    return (f"{spec_desc(config, spec, spec.rows)}; ToGraph + PageRank x{iterations} fp64"
+            f"{' + triangles on the symmetrised graph' if has_tc(spec) else ''}")
 
 
 # ------------------------------------------------------------------ reference
 
-def run_cpu_sample(spec, rows, iterations):
-    """The reference algorithm (oracle port, all host cores) on rows [0, rows)."""
-    from oracle import reference_port as ref
+REF_DIR = REPO / "baseline" / "_ref"
+
+
+def reference_sample(config, scale_cap):
+    """The bounded sample the reference is timed on: the config's own
+    generator family at a smaller size — R-MAT with the same a/b/c, seed, id
+    permutation and edge factor (rows / 2^scale) at scale `scale_cap`; for
+    the uniform C5, the same edge factor over 2^scale_cap ids. The
+    reference's per-row cost grows with graph size (its triangle count most),
+    so a rate measured on the sample overstates its rate on the full table:
+    the GPU/CPU ratio is a lower bound."""
+    from paper_1503_07881_b200.synth import RmatSpec, UniformSpec
+
+    spec = spec_for(config)
+    if isinstance(spec, UniformSpec):
+        n = min(spec.n_nodes, 1 << scale_cap)
+        rows = int(round(spec.rows * n / spec.n_nodes))
+        return UniformSpec(n_nodes=n, rows=rows, seed=spec.seed)
+    scale = min(scale_cap, spec.scale)
+    rows = int(round(spec.rows * (1 << scale) / (1 << spec.scale)))
+    return RmatSpec(scale=scale, rows=rows, a=spec.a, b=spec.b, c=spec.c, seed=spec.seed,
+                    permute=spec.permute)
+
+
+def load_reference():
+    """The unmodified reference package from baseline/_ref (pip --target
+    install of /root/reference/pkg), or None when it is not installed."""
+    if not (REF_DIR / "graphtables" / "__init__.py").exists():
+        return None
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import graphtables
+
+    return graphtables
+
+
+def run_reference_step(spec, iterations, src=None, dst=None):
+    """One step of the path through the reference's public API
+    (convert.py:128, algorithms.py:36/90) with workers=None (all cores), or
+    through the numpy port when the reference is not installed."""
     from paper_1503_07881_b200.synth import spec_edges
 
-    src, dst = spec_edges(spec, rows)
+    if src is None:
+        src, dst = spec_edges(spec)
+    ref = load_reference()
     t0 = time.perf_counter()
-    g = ref.build_csr(src, dst)
-    t1 = time.perf_counter()
-    ref.pagerank_csr(g, 0.85, iterations)
-    t2 = time.perf_counter()
-    tc = ref.triangle_count_csr(g) if has_tc(spec) else None
+    if ref is not None:
+        table = ref.ColumnTable(ref.Schema([("src", "int"), ("dst", "int")]), [src, dst])
+        g = ref.table_to_graph(table, ref.EdgeSpec("src", "dst"))
+        t1 = time.perf_counter()
+        ref.pagerank(g, 0.85, iterations)
+        t2 = time.perf_counter()
+        tc = ref.triangle_count(g) if has_tc(spec) else None
+        n, e, kind = g.node_count, g.edge_count, "reference"
+    else:
+        from oracle import reference_port as port
+
+        g = port.build_csr(src, dst)
+        t1 = time.perf_counter()
+        port.pagerank_csr(g, 0.85, iterations)
+        t2 = time.perf_counter()
+        tc = port.triangle_count_csr(g) if has_tc(spec) else None
+        n, e, kind = g.n, g.e, "port"
     t3 = time.perf_counter()
-    return {"rows": rows, "n": g.n, "e": g.e, "tc": tc, "build_s": t1 - t0, "pr_s": t2 - t1,
-            "tc_s": t3 - t2, "total_s": t3 - t0}
+    return {"rows": int(src.shape[0]), "n": n, "e": e, "tc": tc, "kind": kind,
+            "build_s": t1 - t0, "pr_s": t2 - t1, "tc_s": t3 - t2, "total_s": t3 - t0}
 
 
 def cpu_info():
@@ -136,34 +238,52 @@ def cpu_info():
     return {"cores": os.cpu_count() or 1, "model": model, "numpy": np.__version__}
 
 
+def sample_desc(config, sample, r, iterations):
+    what = ("graphtables (unmodified reference, baseline/_ref) table_to_graph + pagerank"
+            if r["kind"] == "reference" else "oracle/reference_port.py (numpy port) build + pagerank")
+    return (f"{spec_desc(config + '-family sample', sample, sample.rows)}: {what} x{iterations}"
+            f"{' + triangle_count' if has_tc(sample) else ''}, workers=None (all cores); "
+            f"N={r['n']} E={r['e']} triangles={r['tc']}")
+
+
+def config_dict(args, spec, world, n=None, e=None, tc=None):
+    """The `config` object both arms print (same workload, same keys)."""
+    return {"workload": workload_desc(args.config, spec, args.iterations),
+            "rows": spec.rows, "pagerank_iterations": args.iterations,
+            "parallelism": f"sharded x{world} (NCCL)" if world > 1 else "single",
+            "nodes": n, "edges": e, "triangles": tc,
+            "l2": "inputs larger than L2 (16*rows bytes >> 126 MB)"}
+
+
 def reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     spec = spec_for(args.config)
-    rows = min(args.cpu_sample_rows, spec.rows)
+    sample = reference_sample(args.config, args.cpu_sample_scale)
+    from paper_1503_07881_b200.synth import spec_edges
+
+    src, dst = spec_edges(sample)
     for _ in range(args.warmup):
-        run_cpu_sample(spec, rows, args.iterations)
+        run_reference_step(sample, args.iterations, src, dst)
     times = []
     last = None
     for _ in range(args.steps):
-        last = run_cpu_sample(spec, rows, args.iterations)
+        last = run_reference_step(sample, args.iterations, src, dst)
         times.append(last["total_s"])
     mean = sum(times) / len(times)
-    value = rows / mean
+    value = sample.rows / mean
     info = cpu_info()
-    sample = (f"rows [0,{rows}) of {spec_desc(args.config, spec, spec.rows)}: build + PageRank "
-              f"x{args.iterations}{' + triangles' if has_tc(spec) else ''}; "
-              f"N={last['n']} E={last['e']}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} sample", "rows": rows,
-                   "pagerank_iterations": args.iterations},
+        "n_gpus": max(world, args.gpus), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic (seeded, host numpy)",
+        "config": config_dict(args, spec, max(world, args.gpus)),
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": info["cores"],
-                         "kind": "port", "sample": sample, "cpu": info["model"],
+                         "kind": last["kind"], "sample": sample_desc(args.config, sample, last,
+                                                                     args.iterations),
+                         "cpu": info["model"], "numpy": info["numpy"],
                          "phases_s": {k: last[k] for k in ("build_s", "pr_s", "tc_s")}},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -379,25 +499,92 @@ class ClockSampler:
                 "source": "nvml" if self.thread is not None else "nvidia-smi"}
 
 
+def roofline_block(args, phases, steps, rows, n, e, world, pk, elapsed_ms):
+    """HBM roofline of the north-star kernels, per GPU.
+
+    * build: B_kern = the element-count bytes each build kernel is credited
+      with (its contract I/O: DESIGN.md §4.1), and B_min = 16R + 8N +
+      2(8(N+1) + 4E) (read both columns once, write ids and both CSRs);
+    * PageRank: B_PR = 12E + 32N per iteration (int32 in-adjacency + fp64
+      gather per edge; offsets, 1/outdeg, score and contrib per node),
+      over the iteration kernels' time and over the whole call;
+    * the top-level kernel fields are the longest-running HBM-bound kernel of
+      those phases; its `traffic` is ncu dram__bytes per launch from the
+      committed C4 capture (profiles/ncu_traffic.json) when one matches;
+    * triangles: issue-bound (bitmap / hash probes in shared memory), no HBM
+      fraction is claimed; see `phases.triangles`.
+    At N > 1 the bytes are per GPU (R/N rows, E/N edges, N/N rows of PR)."""
+    peak = pk["hbm_gbs"]
+
+    def grp(prefixes, exclude=()):
+        ms = sum(v[0] for k, v in phases.items()
+                 if k.startswith(prefixes) and not k.startswith(exclude)) / steps
+        by = sum(v[2] for k, v in phases.items()
+                 if k.startswith(prefixes) and not k.startswith(exclude)) / steps
+        return ms, by
+
+    g = max(world, 1)
+    b_ms, b_kern = grp(("build.", "sort.", "dist."), exclude=("build.h2d",))
+    b_min = (16.0 * rows + 8.0 * n + 2 * (8.0 * (n + 1) + 4.0 * e)) / g
+    pr_ms, _ = grp(("pr.",))
+    it_ms, _ = grp(("pr.spmv", "pr.fixup", "pr.step"))
+    b_pr = (12.0 * e + 32.0 * n) * args.iterations / g
+    out = {"bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": pk["source"],
+           "phases": {}}
+
+    def frac(by, ms):
+        return (by / (ms / 1e3) / 1e9 / peak) if ms > 0 else None
+
+    out["phases"]["build"] = {
+        "ms": b_ms, "b_kern_gb": b_kern / 1e9, "b_min_gb": b_min / 1e9,
+        "achieved_gbs": b_kern / (b_ms / 1e3) / 1e9 if b_ms else None,
+        "frac": frac(b_kern, b_ms), "compulsory_frac": frac(b_min, b_ms)}
+    out["phases"]["pagerank"] = {
+        "ms": pr_ms, "iterations_ms": it_ms, "b_pr_gb_per_iteration": b_pr / args.iterations / 1e9,
+        "achieved_gbs": b_pr / (it_ms / 1e3) / 1e9 if it_ms else None,
+        "frac": frac(b_pr, it_ms), "frac_whole_call": frac(b_pr, pr_ms)}
+    t_ms, _ = grp(("tc.",))
+    out["phases"]["triangles"] = {
+        "ms": t_ms, "bound": "issue (informational)",
+        "note": "probes are shared-memory bitmap/hash lookups: no HBM fraction claimed; "
+                "ncu sm__throughput and instruction counts in profiles/"}
+    hbm = {k: v for k, v in phases.items()
+           if k.startswith(("build.", "sort.", "pr.", "dist.")) and not k.startswith("build.h2d")
+           and v[2] > 0}
+    if hbm:
+        name, (ms, cnt, by) = max(hbm.items(), key=lambda kv: kv[1][0])
+        ach = by / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+        tr = ncu_traffic(args.config, name)
+        out.update({"kernel": name, "achieved": ach, "frac": ach / peak,
+                    "traffic": (tr or {}).get("bytes_per_launch"), "traffic_source": tr,
+                    "bytes_per_launch": by / max(cnt, 1), "ms_per_launch": ms / max(cnt, 1),
+                    "share_of_step": (ms / steps) / (elapsed_ms / steps)})
+    return out
+
+
 def ours_arm(args):
     import torch
 
     rank, world, local = dist_env()
     os.environ["GT_DEVICE"] = str(local)
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=dev)
+        print(f"[bench rank {rank}/{world}] NCCL process group up on cuda:{local} "
+              f"(nccl {'.'.join(map(str, torch.cuda.nccl.version()))})", file=sys.stderr,
+              flush=True)
 
     import paper_1503_07881_b200 as gt
     from paper_1503_07881_b200 import _native
     from paper_1503_07881_b200.synth import rmat_device
 
     spec = spec_for(args.config)
-    dev = torch.device("cuda", local)
-    # weak scaling: rank r holds rows [r*R, (r+1)*R) of one R-MAT table
-    src, dst = rmat_device(spec, device=f"cuda:{local}", start=rank * spec.rows, rows=spec.rows)
+    # strong scaling: rank r holds rows [rR/N, (r+1)R/N) of the config's table
+    lo, hi = shard_range(rank, world, spec.rows)
+    src, dst = rmat_device(spec, device=f"cuda:{local}", start=lo, rows=hi - lo)
     table = gt.edge_table(src, dst)
     edge_spec = gt.EdgeSpec("src", "dst")
     stream = torch.cuda.ExternalStream(_native.stream_handle(), device=dev)
@@ -423,7 +610,8 @@ def ours_arm(args):
             else:
                 gt.pagerank_device(g, 0.85, iters, out.data_ptr())
                 tc = gt.triangle_count(g) if with_tc else None
-            state.update(n=g.node_count, e=g.edge_count, tc=tc)
+            state.update(n=g.node_count, e=g.edge_count, tc=tc,
+                         m=_native.undirected_edges(g.handle) if with_tc else None)
             del g
     else:
         from paper_1503_07881_b200 import distributed as D
@@ -447,6 +635,15 @@ def ours_arm(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    def max_over_ranks(x):
+        if world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([x], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return x
+
     # ---- timed region: K steps, CUDA events on the library stream ----------
     _native.profile_enable(True)
     _native.profile_reset()
@@ -462,59 +659,40 @@ def ours_arm(args):
         ev1.synchronize()
         barrier()
     launches = _native.launch_count() - launches0
-    elapsed_ms = ev0.elapsed_time(ev1)
+    elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
     phases = _native.profile_read()
     _native.profile_enable(False)
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
 
     rows = spec.rows
     ms_per_step = elapsed_ms / args.steps
-    value = rows * world / (ms_per_step / 1e3)
+    value = rows / (ms_per_step / 1e3)
     n, e, tc = state["n"], state["e"], state["tc"]
+    m_und = state.get("m")
 
     pk = peaks()
 
     def group(prefixes):
         ms = sum(v[0] for k, v in phases.items() if k.startswith(prefixes)) / args.steps
-        by = sum(v[2] for k, v in phases.items() if k.startswith(prefixes)) / args.steps
-        return ms, by
+        return ms
 
-    b_ms, b_bytes = group(("build.", "sort.", "dist."))
-    p_ms, p_bytes = group(("pr.",))
-    t_ms, t_bytes = group(("tc.",))
+    b_ms = group(("build.", "sort.", "dist."))
+    p_ms = group(("pr.",))
+    t_ms = group(("tc.",))
     phase_line = {
-        "build": {"ms": b_ms, "value": rows / (b_ms / 1e3) if b_ms else None, "unit": "rows/s",
-                  "achieved_gbs": b_bytes / (b_ms / 1e3) / 1e9 if b_ms else None},
+        "build": {"ms": b_ms, "value": rows / (b_ms / 1e3) if b_ms else None, "unit": "rows/s"},
         "pagerank": {"ms": p_ms, "value": e * iters / (p_ms / 1e3) if p_ms else None,
-                     "unit": "edge-iterations/s",
-                     "achieved_gbs": p_bytes / (p_ms / 1e3) / 1e9 if p_ms else None},
-        "triangles": {"ms": t_ms, "unit": "undirected edges/s (directed E_d/s in e_d_value)",
+                     "unit": "edge-iterations/s"},
+        "triangles": {"ms": t_ms, "unit": "undirected edges/s (m / t_TC)",
+                      "value": m_und / (t_ms / 1e3) if t_ms and m_und else None,
                       "e_d_value": e / (t_ms / 1e3) if t_ms else None,
-                      "triangles": tc},
+                      "e_d_unit": "directed E_d/s (reference bench unit)",
+                      "triangles": tc, "undirected_edges": m_und},
     }
-    for k in ("build", "pagerank"):
-        if phase_line[k]["achieved_gbs"]:
-            phase_line[k]["hbm_frac"] = phase_line[k]["achieved_gbs"] / pk["hbm_gbs"]
-
     kernels = {}
     for name, (ms, cnt, by) in phases.items():
         kernels[name] = {"ms_per_step": ms / args.steps, "launches_per_step": cnt / args.steps,
                          "gbs": (by / (ms / 1e3) / 1e9) if ms > 0 and by > 0 else None}
-    dom_name, (dom_ms, dom_cnt, dom_bytes) = max(phases.items(), key=lambda kv: kv[1][0])
-    dom_gbs = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
-    roofline = {"bound": "hbm", "kernel": dom_name,
-                "achieved": dom_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": dom_gbs / pk["hbm_gbs"],
-                "traffic": (ncu_traffic(args.config, dom_name) or {}).get("bytes_per_launch"),
-                "traffic_source": ncu_traffic(args.config, dom_name),
-                "bytes_per_launch": dom_bytes / max(dom_cnt, 1),
-                "ms_per_launch": dom_ms / max(dom_cnt, 1), "peak_source": pk["source"],
-                "share_of_step": dom_ms / elapsed_ms}
+    roofline = roofline_block(args, phases, args.steps, rows, n, e, world, pk, elapsed_ms)
 
     # ---- §8f next #1: graph -> edge table export (device), measured apart ----
     extras = {}
@@ -583,8 +761,9 @@ def ours_arm(args):
     # ---- end to end through the public API with host buffers ---------------
     e2e = None
     if not args.no_e2e:
-        h_src = torch.empty(rows, dtype=torch.int64, pin_memory=True)
-        h_dst = torch.empty(rows, dtype=torch.int64, pin_memory=True)
+        my_rows = hi - lo
+        h_src = torch.empty(my_rows, dtype=torch.int64, pin_memory=True)
+        h_dst = torch.empty(my_rows, dtype=torch.int64, pin_memory=True)
         h_src.copy_(src)
         h_dst.copy_(dst)
         host_table = gt.edge_table(h_src.numpy(), h_dst.numpy())
@@ -599,13 +778,11 @@ def ours_arm(args):
                 # HBM, side stream) while the previous step computed; the next
                 # step's copy is issued now and overlaps this step's PageRank
                 # and triangle count
-                t0_ = time.perf_counter()
                 cur = pipe["next"] if pipe["next"] is not None else host_table.prefetch()
                 g = gt.table_to_graph(cur, edge_spec)
                 del cur
                 if not os.environ.get("BENCH_E2E_SERIAL"):
                     pipe["next"] = host_table.prefetch()
-                t1_ = time.perf_counter()
                 # scores stay in HBM until the count is done, then one D2H read:
                 # a read issued while the next table's H2D copy is in flight
                 # waited for that copy (C4: +410 ms), one after the count does not
@@ -618,17 +795,12 @@ def ours_arm(args):
                 if with_tc and args.lanes:
                     _, tc_ = gt.pagerank_and_triangles(g, 0.85, iters,
                                                        scores_out_ptr=d_sc.data_ptr())
-                    t2_ = time.perf_counter()
                 else:
                     gt.pagerank_device(g, 0.85, iters, d_sc.data_ptr())
-                    t2_ = time.perf_counter()
                     tc_ = gt.triangle_count(g) if with_tc else None
                 pipe["flip"] = 1 - pipe.get("flip", 0)
                 pr = pipe["h_sc"][pipe["flip"]][:n_]
                 pr.copy_(d_sc[:n_])  # device -> pinned host, synchronous
-                if os.environ.get("BENCH_E2E_DEBUG"):
-                    print(f"e2e split: build {1e3 * (t1_ - t0_):.1f} pr {1e3 * (t2_ - t1_):.1f} "
-                          f"tc {1e3 * (time.perf_counter() - t2_):.1f} ms", file=sys.stderr)
                 return pr, tc_
         else:
             def e2e_step():
@@ -658,52 +830,42 @@ def ours_arm(args):
         torch.cuda.synchronize()  # the copy issued by the last step completes inside the region
         wall = time.perf_counter() - t0
         barrier()
-        e2e_ms = max(e0.elapsed_time(e1), wall * 1e3) / args.steps
-        if world > 1:
-            import torch.distributed as dist
-
-            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), wall * 1e3) / args.steps)
         assert tc2 == tc, "e2e triangle count differs from the device-resident run"
-        e2e = {"value": rows * world / (e2e_ms / 1e3), "unit": "rows/s",
+        e2e = {"value": rows / (e2e_ms / 1e3), "unit": "rows/s",
                "ms_per_step": e2e_ms, "h2d_bytes_per_step": 16 * rows,
                "pipelined": (None if sharded else
                              "ColumnTable.prefetch: each step's table is copied from pinned "
                              "host memory on a side stream while the previous step computes; "
                              "one copy per timed step, all inside the timed region"),
-               "d2h_bytes_per_step": (8 * n + 8) if not sharded else 16 * n + 8 + 8,
+               "d2h_bytes_per_step": (8 * n + 8) if not sharded else (8 * n + 8) * world,
                "api": (("host ColumnTable.prefetch -> table_to_graph -> pagerank_device"
-                        if not sharded else "table_to_graph(host ColumnTable) -> pagerank")
+                        if not sharded else "distributed.build_csr(host slice) -> pagerank")
                        + (" -> triangle_count" if with_tc else "")
                        + (" -> scores to pinned host" if not sharded else ""))}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = run_cpu_sample(spec, min(args.cpu_sample_rows, rows), iters)
+        sample = reference_sample(args.config, args.cpu_sample_scale)
+        from paper_1503_07881_b200.synth import spec_edges
+
+        s_src, s_dst = spec_edges(sample)
+        reps = [run_reference_step(sample, iters, s_src, s_dst) for _ in range(2)]
+        tot = sum(r["total_s"] for r in reps)
         info = cpu_info()
-        cpu = {"value": r["rows"] / r["total_s"], "unit": "rows/s", "cores": info["cores"],
-               "kind": "port",
-               "sample": (f"rows [0,{r['rows']}) of {args.config}: build + PageRank x{iters}"
-                          f"{' + triangles' if with_tc else ''} via oracle/reference_port.py "
-                          f"(numpy, workers=all cores), "
-                          f"N={r['n']} E={r['e']}; {r['total_s']:.2f}s"),
+        cpu = {"value": sample.rows * len(reps) / tot, "unit": "rows/s", "cores": info["cores"],
+               "kind": reps[-1]["kind"],
+               "sample": sample_desc(args.config, sample, reps[-1], iters)
+                         + f"; {len(reps)} reps, {tot:.2f} s",
                "cpu": info["model"],
-               "phases_s": {k: r[k] for k in ("build_s", "pr_s", "tc_s")}}
+               "phases_s": {k: reps[-1][k] for k in ("build_s", "pr_s", "tc_s")}}
 
     line = {
         "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "int64+f64", "data": "synthetic (generated on device, seeded)",
-        "config": {"workload": f"{spec_desc(args.config, spec, rows * world)}; ToGraph + "
-                               f"PageRank x{iters} fp64"
-                               f"{' + triangles (C3)' if with_tc else ''}",
-                   "rows": rows, "nodes": n, "edges": e, "triangles": tc,
-                   "pagerank_iterations": iters,
-                   "parallelism": f"sharded x{world} (NCCL)" if sharded else "single",
-                   "rows_per_gpu": rows,
-                   "l2": "inputs larger than L2 (16*rows bytes >> 126 MB)"},
+        "config": config_dict(args, spec, world, n, e, tc),
         "phases": phase_line, "extras": extras, "kernels": kernels, "roofline": roofline,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks.summary(),
@@ -735,6 +897,7 @@ def ncu_traffic(config, phase):
 
 def main():
     args = parse_args()
+    maybe_reexec(args)
     if args.impl == "reference":
         return reference_arm(args)
     return ours_arm(args)

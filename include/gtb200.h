@@ -330,6 +330,10 @@ GT_API int gt_pagerank_step(const int64_t* d_in_off, const int32_t* d_in_adj, in
  * the rank-space orientation: the parts of all ranks sum to gt_triangles
  * (the all-reduce is the caller's). */
 GT_API int gt_triangles_part(const gt_graph* g, int part, int nparts, int64_t* count);
+/* Undirected simple-edge count m of the graph (self-loops dropped, reciprocal
+ * pairs merged: the size of the orientation the triangle count builds), or -1
+ * when no triangle count has run on g yet (bench unit: undirected edges/s). */
+GT_API int gt_graph_undirected_edges(const gt_graph* g, int64_t* m);
 
 /* ---- instrumentation ---------------------------------------------------- */
 

@@ -88,6 +88,7 @@ SIGNATURES = {
                                         _VP, _VP, _VP, ctypes.c_double, ctypes.c_int, _VP, _VP,
                                         _VP]),
     "gt_triangles_part": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, _I64P]),
+    "gt_graph_undirected_edges": (ctypes.c_int, [_VP, _I64P]),
     "gt_select_rows": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int64, ctypes.c_double, _VP, ctypes.c_int64, _VP,
                                       _I64P]),
@@ -157,7 +158,28 @@ def ensure_init():
     if not _initialised:
         check(lib.gt_init(device_ordinal()), "gt_init")
         _initialised = True
+    order_after_torch()
     return lib
+
+
+def order_after_torch():
+    """Order the library stream after the caller's torch stream.
+
+    The library's streams are blocking streams, so they already run after
+    everything queued on torch's default (legacy) stream. When the caller
+    works on another torch stream (``with torch.cuda.stream(s)``), make the
+    library stream wait on it here, so that buffers written by torch ops are
+    complete before a library kernel reads them. Called by every entry point
+    (via ``ensure_init``)."""
+    import sys
+
+    torch = sys.modules.get("torch")
+    if torch is None or not torch.cuda.is_initialized():
+        return
+    cur = torch.cuda.current_stream()
+    if cur.cuda_stream == 0:
+        return
+    torch.cuda.ExternalStream(load().gt_stream(), device=cur.device).wait_stream(cur)
 
 
 def _ptr(a: np.ndarray) -> int:
@@ -260,6 +282,13 @@ def triangles(handle: int) -> int:
     c = ctypes.c_int64()
     check(lib.gt_triangles(handle, ctypes.byref(c)), "gt_triangles")
     return int(c.value)
+
+
+def undirected_edges(handle: int) -> int:
+    """m of the last triangle count on this graph (-1 before the first)."""
+    m = ctypes.c_int64()
+    check(load().gt_graph_undirected_edges(handle, ctypes.byref(m)), "gt_graph_undirected_edges")
+    return int(m.value)
 
 
 def bfs(handle: int, n: int, source_index: int) -> np.ndarray:

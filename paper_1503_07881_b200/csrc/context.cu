@@ -27,20 +27,29 @@ static Context g_lanes[GT_LANES];
 static thread_local int t_lane = 0;
 static std::atomic<bool> g_profiling{false};
 static std::mutex g_init_mu;
+static int init_locked(int device);  // gt_init body; caller holds g_init_mu
 Context& ctx() { return g_lanes[t_lane]; }
+
+// Library streams are created BLOCKING (no cudaStreamNonBlocking): work on
+// them is ordered after everything queued before on the legacy default
+// stream — torch's default stream — so device buffers a caller just wrote
+// with torch ops are complete before a library kernel reads them. (Callers on
+// another stream order themselves: the Python layer waits on it, see
+// _native.order_after_torch.)
+static constexpr unsigned kStreamFlags = cudaStreamDefault;
 
 void require_init() {
   if (ctx().stream != nullptr) return;
+  std::lock_guard<std::mutex> lk(g_init_mu);
   if (g_lanes[0].stream == nullptr) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
     const int lane = t_lane;
     t_lane = 0;
-    const int rc = gt_init(dev);
+    const int rc = init_locked(dev);
     t_lane = lane;
     if (rc != GT_OK) fail(GT_ENODEV, std::string("gt_init failed: ") + g_last_error);
   }
-  std::lock_guard<std::mutex> lk(g_init_mu);
   Context& c = ctx();
   if (c.stream == nullptr) {  // a further lane: lane 0's device, its own stream
     const Context& z = g_lanes[0];
@@ -49,7 +58,7 @@ void require_init() {
     c.sm_count = z.sm_count;
     c.l2_bytes = z.l2_bytes;
     c.smem_optin = z.smem_optin;
-    GT_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    GT_CUDA(cudaStreamCreateWithFlags(&c.stream, kStreamFlags));
   }
 }
 
@@ -189,13 +198,7 @@ Phase::~Phase() {
   g_phases[idx].pending.emplace_back(start, end);
 }
 
-}  // namespace gt
-
-using namespace gt;
-
-extern "C" {
-
-int gt_init(int device) {
+static int init_locked(int device) {
   try {
     Context& c = ctx();
     if (c.stream != nullptr && c.device == device) return GT_OK;
@@ -205,6 +208,15 @@ int gt_init(int device) {
       fail(GT_ENODEV, "no CUDA device visible (libgtb200 has no CPU fallback)");
     }
     if (device < 0 || device >= n) fail(GT_EINVAL, "device ordinal out of range");
+    if (c.stream != nullptr) {
+      // switching devices: this lane's workspace and stream belong to the old
+      // one — release them there before re-initialising
+      GT_CUDA(cudaSetDevice(c.device));
+      ws_release_all();
+      GT_CUDA(cudaStreamSynchronize(c.stream));
+      GT_CUDA(cudaStreamDestroy(c.stream));
+      c.stream = nullptr;
+    }
     GT_CUDA(cudaSetDevice(device));
     cudaDeviceProp prop;
     GT_CUDA(cudaGetDeviceProperties(&prop, device));
@@ -218,7 +230,7 @@ int gt_init(int device) {
     c.sm_count = prop.multiProcessorCount;
     c.l2_bytes = prop.l2CacheSize;
     c.smem_optin = int(prop.sharedMemPerBlockOptin);
-    GT_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    GT_CUDA(cudaStreamCreateWithFlags(&c.stream, kStreamFlags));
     cudaMemPool_t pool;
     GT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t threshold = UINT64_MAX;
@@ -228,6 +240,17 @@ int gt_init(int device) {
     set_last_error(e.what());
     return e.code;
   }
+}
+
+}  // namespace gt
+
+using namespace gt;
+
+extern "C" {
+
+int gt_init(int device) {
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  return init_locked(device);
 }
 
 const char* gt_version(void) { return "gtb200 0.1.0 (sm_100a)"; }

@@ -21,6 +21,8 @@ struct gt_graph {
   int32_t* out_adj = nullptr;
   int64_t* in_off = nullptr;
   int32_t* in_adj = nullptr;
+  // undirected simple-edge count m, set by the first triangle count (-1 before)
+  mutable int64_t m_und = -1;
 };
 
 namespace gt {

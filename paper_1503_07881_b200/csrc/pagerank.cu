@@ -483,14 +483,16 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
   }
   // L2 residency for the hot sources: after the relabelling the first
   // positions of the contrib vector are the high out-degree sources; when the
-  // vector is larger than what L2 keeps on its own, an access-policy window
-  // marks its hot head as persisting for the gathers of each iteration.
+  // vector is larger than what L2 keeps on its own, the tail gathers carry an
+  // L2 cache policy: the hot head evict_last, the rest evict_first.
   const size_t contrib_bytes = size_t(n) * 8;
-  size_t window = 0;
   uint32_t hot_bytes = 0, total_bytes = 0;
-  static const int l2_mode = [] {  // GT_PR_L2: "policy" (default), "window", "none"
+  // GT_PR_L2: "policy" (default) or "none". (A persisting access-policy
+  // window was dropped: its set-up and release act on the whole device and
+  // synchronise it, stalling the other lane and resetting its L2 set-aside.)
+  static const int l2_mode = [] {
     const char* v = getenv("GT_PR_L2");
-    return (v && !strcmp(v, "window")) ? 1 : (v && !strcmp(v, "none")) ? 2 : 0;
+    return (v && !strcmp(v, "none")) ? 2 : 0;
   }();
   if (contrib_bytes > ctx().l2_bytes / 2 && l2_mode == 0 && contrib_bytes < (size_t(1) << 32)) {
     int max_win = 0;
@@ -500,29 +502,10 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
     hot_bytes = uint32_t(std::min<size_t>({contrib_bytes, size_t(max_win), size_t(persist_max)}));
     total_bytes = uint32_t(contrib_bytes);
   }
-  if (contrib_bytes > ctx().l2_bytes / 2 && l2_mode == 1) {
-    int max_win = 0;
-    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, ctx().device);
-    int persist_max = 0;
-    cudaDeviceGetAttribute(&persist_max, cudaDevAttrMaxPersistingL2CacheSize, ctx().device);
-    window = std::min<size_t>({contrib_bytes, size_t(max_win), size_t(persist_max)});
-    if (window > 0) GT_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, window));
-  }
-  auto set_window = [&](const double* base) {
-    if (window == 0) return;
-    cudaStreamAttrValue attr = {};
-    attr.accessPolicyWindow.base_ptr = const_cast<double*>(base);
-    attr.accessPolicyWindow.num_bytes = window;
-    attr.accessPolicyWindow.hitRatio = 1.0f;
-    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    GT_CUDA(cudaStreamSetAttribute(ctx().stream, cudaStreamAttributeAccessPolicyWindow, &attr));
-  };
   for (int it = 0; it < iterations; ++it) {
     const int last = it == iterations - 1;
     double* cur = contrib[it & 1];
     double* nxt = contrib[(it + 1) & 1];
-    set_window(cur);
     {
       Phase ph("pr.spmv", 12.0 * e + 8.0 * (n + 1) + 20.0 * n);
       GT_LAUNCH(gtd::pr_spmv_kernel, static_cast<int>(tiles), gtd::PR_THREADS, 0, g->in_off,
@@ -535,15 +518,6 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
                 dang + it, damping, head, tail, tail_row, dpart, score, nxt, last, partials,
                 ticket, dang + it + 1);
     }
-  }
-  if (window) {  // release the persisting lines, the stream's window AND the set-aside:
-    // a persisting carve-out left in place measured ~140 ms slower on the
-    // following build and triangle kernels at C4
-    cudaStreamAttrValue attr = {};
-    attr.accessPolicyWindow.num_bytes = 0;
-    GT_CUDA(cudaStreamSetAttribute(ctx().stream, cudaStreamAttributeAccessPolicyWindow, &attr));
-    GT_CUDA(cudaCtxResetPersistingL2Cache());
-    GT_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
   }
   if (!on_device) {
     d2h(scores, score, size_t(n) * 8);

@@ -1516,6 +1516,7 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
   uint32_t* counters = ws_n<uint32_t>(WS_COUNTERS, 64);
   const Oriented o = orient(g);
   const int64_t m = o.m;
+  g->m_und = m;
   if (m == 0) return 0;
   if (m >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangles: >= 2^31 undirected edges");
 
@@ -1590,7 +1591,7 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
     // algorithmic bytes: every probed suffix element (2 B for the bitmap
     // tasks, which read adj16, 4 B otherwise), the N- entries (8 B) and the N+
     // lists loaded into tables (4 B); hash tasks counted here too
-    Phase ph("tc.count", 2.0 * double(probes_bm) + 4.0 * double(probes - probes_bm) + 12.0 * m);
+    Phase ph("tc.count", 0.0);  // issue-bound probes: no HBM bytes claimed
     GT_CUDA(cudaMemsetAsync(counters + 22, 0, 4, s));
     const int smem = 8 * gtd::TC_SLOTS * 4;
     GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_warp_kernel,
@@ -1650,6 +1651,13 @@ int gt_triangles(const gt_graph* g, int64_t* count) {
   GT_API_BEGIN
   if (!count) fail(GT_EINVAL, "count must not be NULL");
   *count = triangles(g, 0, 1);
+  GT_API_END
+}
+
+int gt_graph_undirected_edges(const gt_graph* g, int64_t* m) {
+  GT_API_BEGIN
+  if (!g || !m) fail(GT_EINVAL, "graph and m must not be NULL");
+  *m = g->m_und;
   GT_API_END
 }
 

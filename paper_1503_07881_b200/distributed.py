@@ -112,9 +112,9 @@ class NativeOps:
     def sort_keys(self, keys, lo_bit, hi_bit):
         import ctypes
 
-        self._pre()
-        keys = keys.contiguous().clone()
+        keys = keys.contiguous().clone()  # torch-stream copy: ordered before the sort by _pre
         tmp = torch.empty_like(keys)
+        self._pre()
         which = ctypes.c_int()
         self._ck(self.lib.gt_sort_keys(keys.data_ptr(), tmp.data_ptr(), keys.numel(), lo_bit,
                                        hi_bit, ctypes.byref(which)), "gt_sort_keys")
