@@ -298,6 +298,25 @@ static gt_graph* empty_graph() {
   return g;
 }
 
+// Shared with bucket_build.cu.
+void launch_presence(const int64_t* a, const int64_t* b, int64_t n, int64_t lo, uint2* words) {
+  if (n) GT_LAUNCH(gtd::presence_kernel, grid_for(n, 4), 256, 0, a, b, n, lo, words);
+}
+void launch_word_prefix(uint2* words, int64_t nw, int64_t* total_out) {
+  const int64_t tiles = ceil_div64(nw, 256 * 16);
+  uint64_t* status = ws_n<uint64_t>(WS_LOOKBACK, size_t(tiles) * 256);
+  uint32_t* counters = ws_n<uint32_t>(WS_COUNTERS, 64);
+  GT_CUDA(cudaMemsetAsync(counters + 16, 0, 4, ctx().stream));
+  GT_LAUNCH(gtd::word_prefix_kernel, static_cast<int>(tiles), 256, 0, words, nw, status,
+            counters + 16, next_epoch(), total_out);
+}
+void launch_ids(const uint2* words, int64_t nw, int64_t lo, int64_t* ids) {
+  GT_LAUNCH(gtd::ids_kernel, ceil_div(nw, 256), 256, 0, words, nw, lo, ids);
+}
+bool bucket_build_applies(int64_t rows, uint64_t span);
+void bucket_build(const int64_t* src, const int64_t* dst, int64_t rows, const int64_t* extra,
+                  int64_t n_extra, int64_t lo, uint64_t span, gt_graph* g);
+
 void graph_free(gt_graph* g) {
   if (!g) return;
   dfree(g->ids);
@@ -350,6 +369,10 @@ gt_graph* build_csr(const int64_t* src, const int64_t* dst, int64_t rows, const 
     const bool dense = span < (uint64_t(1) << 36) &&
                        (span + 1) <= std::max<uint64_t>(uint64_t(1) << 26, uint64_t(rows) * 32);
 
+    if (dense && bucket_build_applies(rows, span)) {
+      bucket_build(src, dst, rows, extra, n_extra, lo, span, g);
+      return g;
+    }
     uint2* words = nullptr;
     int64_t nw = 0;
     int64_t n_nodes = 0;

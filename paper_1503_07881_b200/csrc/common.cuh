@@ -186,4 +186,46 @@ __device__ __forceinline__ uint64_t lookback_single(uint64_t* status, int tile, 
   return excl;
 }
 
+// Warp-parallel decoupled look-back (called by all 32 lanes of ONE warp):
+// 32 predecessors polled per round trip, consumed up to the nearest
+// inclusive value (or up to the first one not yet published). Returns the
+// exclusive prefix of `tile` to every lane and publishes its inclusive value.
+// For chains whose tiles finish out of order (variable-size work units).
+__device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int tile, uint32_t epoch,
+                                                  uint64_t aggregate) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t ep = uint64_t(epoch & 0x3FFFFFu);
+  if (lane == 0)
+    st_status_u64(&status[tile], lb_pack(tile == 0 ? LB_INC : LB_AGG, epoch, aggregate));
+  uint64_t excl = 0;
+  int t = tile - 1;
+  while (t >= 0) {
+    const int idx = t - lane;
+    uint64_t v = idx >= 0 ? ld_status_u64(&status[idx]) : (LB_INC | (ep << 40));
+    const bool ready = ((v >> 40) & 0x3FFFFFu) == ep && (v >> 62) != 0;
+    const uint32_t inc = __ballot_sync(0xffffffffu, ready && (v >> 62) == 2);
+    const uint32_t notready = __ballot_sync(0xffffffffu, !ready);
+    // lanes [0, lim] are needed: up to the nearest inclusive value, else all
+    const int lim = inc ? __ffs(inc) - 1 : 31;
+    const uint32_t need = lim == 31 ? 0xffffffffu : ((2u << lim) - 1u);
+    int take;  // lanes consumed this round
+    bool done;
+    if (notready & need) {
+      take = __ffs(notready & need) - 1;  // all-aggregate prefix before the first gap
+      done = false;
+    } else {
+      take = lim + 1;
+      done = inc != 0;
+    }
+    uint64_t x = lane < take ? (v & ((1ull << 40) - 1)) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    excl += x;
+    t -= take;
+    if (done) break;
+  }
+  if (lane == 0 && tile > 0) st_status_u64(&status[tile], lb_pack(LB_INC, epoch, excl + aggregate));
+  return excl;
+}
+
 }  // namespace gtd
