@@ -282,8 +282,16 @@ def _fast_lib():
         build_oracle()
     lib = ctypes.CDLL(str(path))
     i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+    i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+    f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
     lib.oracle_triangles.restype = ctypes.c_int64
     lib.oracle_triangles.argtypes = [ctypes.c_int64, i64p, i64p, i64p, i64p, ctypes.c_int]
+    lib.oracle_triangles_slice32.restype = ctypes.c_int64
+    lib.oracle_triangles_slice32.argtypes = [ctypes.c_int64, i64p, i32p, i64p, i32p,
+                                             ctypes.c_int64, ctypes.c_int64, ctypes.c_int]
+    lib.oracle_pagerank32.restype = None
+    lib.oracle_pagerank32.argtypes = [ctypes.c_int64, i64p, i32p, i64p, ctypes.c_double,
+                                      ctypes.c_int, f64p, ctypes.c_int]
     return lib
 
 
@@ -296,6 +304,29 @@ def triangle_count_fast(g: CSR, threads: int = 0) -> int:
     in_d = np.ascontiguousarray(np.searchsorted(g.ids, g.in_adj), dtype=np.int64)
     return int(lib.oracle_triangles(g.n, np.ascontiguousarray(g.out_off), out_d,
                                     np.ascontiguousarray(g.in_off), in_d, int(threads)))
+
+
+def triangles_slice_dense32(n, out_off, out_adj, in_off, in_adj, part, nparts, threads=0):
+    """Triangles whose middle vertex in (undirected degree, id) rank order has
+    rank % nparts == part (algorithms.py:103-116 restated in C over the
+    dense int32 CSR pair; the slice gt_triangles_part counts)."""
+    lib = _fast_lib()
+    return int(lib.oracle_triangles_slice32(
+        int(n), np.ascontiguousarray(out_off, np.int64), np.ascontiguousarray(out_adj, np.int32),
+        np.ascontiguousarray(in_off, np.int64), np.ascontiguousarray(in_adj, np.int32),
+        int(part), int(nparts), int(threads)))
+
+
+def pagerank_dense32(n, in_off, in_adj, out_off, damping, iterations, threads=0):
+    """algorithms.py:45-85 in C over the dense int32 in-CSR (scores in dense
+    index order)."""
+    lib = _fast_lib()
+    out = np.empty(int(n), dtype=np.float64)
+    lib.oracle_pagerank32(int(n), np.ascontiguousarray(in_off, np.int64),
+                          np.ascontiguousarray(in_adj, np.int32),
+                          np.ascontiguousarray(out_off, np.int64), float(damping),
+                          int(iterations), out, int(threads))
+    return out
 
 
 # ------------------------------------- algorithms.py:122-248 (§8f next #4)

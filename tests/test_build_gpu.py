@@ -301,4 +301,4 @@ def test_c4_full_size_properties():
         c = ctypes.c_int64()
         _native.check(lib.gt_triangles_part(g.handle, p, 4, ctypes.byref(c)), "gt_triangles_part")
         parts += c.value
-    assert parts == total == 99862871249  # the value every C4 run of this table reports
+    assert parts == total  # exact value: tests/test_large_gpu.py (oracle on a slice)

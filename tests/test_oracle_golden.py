@@ -132,3 +132,26 @@ def test_oracle_updates_match_reference(name):
                          add_nodes=c["add_nodes"], del_nodes=c["del_nodes"])
     for f in ("ids", "out_off", "out_adj", "in_off", "in_adj"):
         assert np.array_equal(getattr(got, f), c[f]), f
+
+
+def _dense32(case):
+    ids = case["ids"]
+    return (np.searchsorted(ids, case["out_adj"]).astype(np.int32),
+            np.searchsorted(ids, case["in_adj"]).astype(np.int32))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_large_size_checkers_match_reference(name):
+    """The int32 checkers used at BASELINE configs[3]/[4] (triangle slices by
+    middle-vertex rank, pull PageRank) reproduce the reference's outputs."""
+    case = golden_cases()[name]
+    n = case["ids"].shape[0]
+    if n == 0:
+        pytest.skip("empty graph")
+    oa, ia = _dense32(case)
+    for nparts in (1, 5):
+        parts = sum(ref.triangles_slice_dense32(n, case["out_off"], oa, case["in_off"], ia, p,
+                                                nparts, threads=2) for p in range(nparts))
+        assert parts == int(case["tc"][0])
+    pr = ref.pagerank_dense32(n, case["in_off"], ia, case["out_off"], 0.85, 10, threads=2)
+    assert np.max(np.abs(pr - case["pr"])) <= 1e-12
