@@ -246,12 +246,12 @@ def sample_desc(config, sample, r, iterations):
             f"N={r['n']} E={r['e']} triangles={r['tc']}")
 
 
-def config_dict(args, spec, world, n=None, e=None, tc=None):
-    """The `config` object both arms print (same workload, same keys)."""
+def config_dict(args, spec, world):
+    """The `config` object both arms print (identical: same workload, same
+    keys; the graph's measured sizes go to `graph` in our arm's line)."""
     return {"workload": workload_desc(args.config, spec, args.iterations),
             "rows": spec.rows, "pagerank_iterations": args.iterations,
             "parallelism": f"sharded x{world} (NCCL)" if world > 1 else "single",
-            "nodes": n, "edges": e, "triangles": tc,
             "l2": "inputs larger than L2 (16*rows bytes >> 126 MB)"}
 
 
@@ -865,7 +865,8 @@ def ours_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "int64+f64", "data": "synthetic (generated on device, seeded)",
-        "config": config_dict(args, spec, world, n, e, tc),
+        "config": config_dict(args, spec, world),
+        "graph": {"nodes": n, "edges": e, "undirected_edges": m_und, "triangles": tc},
         "phases": phase_line, "extras": extras, "kernels": kernels, "roofline": roofline,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks.summary(),

@@ -272,6 +272,11 @@ int gt_release_workspace(void) {
     if (ctx().stream == nullptr) return GT_OK;
     ws_release_all();
     sync();
+    // the pool keeps freed blocks (release threshold raised at init); hand
+    // them back to the driver so other allocators (torch) can use the memory
+    cudaMemPool_t pool;
+    GT_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx().device));
+    GT_CUDA(cudaMemPoolTrimTo(pool, 0));
     return GT_OK;
   } catch (const Error& e) {
     set_last_error(e.what());

@@ -51,13 +51,25 @@ def _views(g):
             "in_adj": as_t(ia_p, e, "<i4").cpu().numpy()}
 
 
+def _free_device_memory():
+    import gc
+
+    import torch
+
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    _native.load().gt_release_workspace()
+
+
 def _build(name):
+    _free_device_memory()
     src, dst = rmat_device(CONFIGS[name])
     g = gt.table_to_graph(gt.edge_table(src, dst), SPEC)
     h = _views(g)
     h["src"], h["dst"] = src.cpu().numpy(), dst.cpu().numpy()
     del src, dst
-    _native.load().gt_release_workspace()
+    _free_device_memory()
     h["g"] = g
     return h
 
