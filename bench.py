@@ -527,7 +527,7 @@ def roofline_block(args, phases, steps, rows, n, e, world, pk, elapsed_ms):
     b_ms, b_kern = grp(("build.", "sort.", "dist."), exclude=("build.h2d",))
     b_min = (16.0 * rows + 8.0 * n + 2 * (8.0 * (n + 1) + 4.0 * e)) / g
     pr_ms, _ = grp(("pr.",))
-    it_ms, _ = grp(("pr.spmv", "pr.fixup", "pr.step"))
+    it_ms, _ = grp(("pr.spmv", "pr.fixup", "pr.step", "pr.finalize"))
     b_pr = (12.0 * e + 32.0 * n) * args.iterations / g
     out = {"bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": pk["source"],
            "phases": {}}

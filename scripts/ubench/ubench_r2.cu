@@ -257,7 +257,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __global__ void __launch_bounds__(128) gather_tma4(const __grid_constant__ CUtensorMap tm,
                                                    const int32_t* __restrict__ idx, int64_t e,
                                                    double* __restrict__ out) {
-  __shared__ __align__(128) double buf[4][2][32 * 8];  // warp, stage, lane*8 doubles
+  __shared__ __align__(128) double buf[4][2][32 * 16];  // warp, stage, lane*16 doubles (128 B)
   __shared__ __align__(8) uint64_t bar[4][2];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) {
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(128) gather_tma4(const __grid_constant__ CUten
     const int4 q = *reinterpret_cast<const int4*>(idx + at + lane * 4);
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(&buf[w][s][lane * 8])),
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(&buf[w][s][lane * 16])),
         "l"(&tm), "r"(0), "r"(q.x >> 1), "r"(q.y >> 1), "r"(q.z >> 1), "r"(q.w >> 1),
         "r"(smem_u32(&bar[w][s]))
         : "memory");
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(128) gather_tma4(const __grid_constant__ CUten
           : "=r"(done) : "r"(smem_u32(&bar[w][s])), "r"(phase[s]) : "memory");
     phase[s] ^= 1;
     const int4 q = *reinterpret_cast<const int4*>(idx + r + lane * 4);
-    const double* b = &buf[w][s][lane * 8];
+    const double* b = &buf[w][s][lane * 16];
     acc += b[0 + (q.x & 1)] + b[2 + (q.y & 1)] + b[4 + (q.z & 1)] + b[6 + (q.w & 1)];
     __syncwarp();
     r = nx;
@@ -404,8 +404,10 @@ int main(int argc, char** argv) {
         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     printf("tensor map encode: %d\n", int(cr));
-    for (int skew = 0; skew < 2; ++skew) {
-      gen_idx<<<sms * 8, 256>>>(idx, e, nn, skew, 7);
+    const int nsk = (argc > 3) ? 3 : 2;
+    for (int skew = 0; skew < nsk; ++skew) {
+      // skew 2: uniform over the first 8M doubles (64 MB: L2-resident)
+      gen_idx<<<sms * 8, 256>>>(idx, e, skew == 2 ? (8 << 20) : nn, skew == 1, 7);
       CK(cudaDeviceSynchronize());
       for (int v = 0; v < 3; ++v) {
         if (v == 2 && (cr != CUDA_SUCCESS || (argc > 2 && !strcmp(argv[2], "notma")))) continue;
@@ -423,7 +425,7 @@ int main(int argc, char** argv) {
           if (rep) best = std::min(best, ms);
         }
         printf("gather %s %s: %.3f ms  %.1f G gathers/s  %.3f gathers/cycle/SM@1.965GHz\n",
-               skew ? "logskew" : "uniform", v == 0 ? "ldg" : v == 1 ? "ldg.na" : "tma.gather4",
+               skew == 2 ? "uniform64MB" : skew ? "logskew" : "uniform", v == 0 ? "ldg" : v == 1 ? "ldg.na" : "tma.gather4",
                best, e / best / 1e6, e / best / 1e6 / (sms * 1.965));
       }
     }

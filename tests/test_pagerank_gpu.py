@@ -122,3 +122,27 @@ def test_c2_full_sum_and_oracle():
                                       ("ids", "out_off", "out_adj", "in_off", "in_adj")]),
                             0.85, 20)
     assert np.abs(got - want).sum() <= L1_TOL
+
+
+@pytest.mark.parametrize("segbits", [10, 13])
+def test_cache_blocked_pull_matches_single_pass(monkeypatch, segbits):
+    """The cache-blocked iteration (source segments of 2^segbits positions,
+    doubly-compressed per-segment in-CSR; used when contrib exceeds L2, i.e.
+    BASELINE configs[3]/[4]) against the single-pass pull and the oracle on
+    a graph with hubs, dangling nodes and self-loops."""
+    from paper_1503_07881_b200.synth import rmat_edges
+
+    src, dst = rmat_edges(16, 600_000, seed=21, permute=True)
+    src = np.concatenate([src, np.arange(50), np.full(3000, 7)])
+    dst = np.concatenate([dst, np.arange(50), np.arange(3000)])
+    t = gt.edge_table(src.astype(np.int64), dst.astype(np.int64))
+    g = gt.table_to_graph(t, gt.EdgeSpec("src", "dst"))
+    single = np.array([v for _, v in sorted(gt.pagerank(g, 0.85, 20).items())])
+    monkeypatch.setenv("GT_PR_BLOCK", "1")
+    monkeypatch.setenv("GT_PR_SEGBITS", str(segbits))
+    blocked = np.array([v for _, v in sorted(gt.pagerank(g, 0.85, 20).items())])
+    assert np.abs(blocked - single).sum() <= 1e-12
+    want = ref.pagerank_csr(ref.build_csr(src.astype(np.int64), dst.astype(np.int64)), 0.85, 20)
+    assert np.abs(blocked - want).sum() <= 1e-9
+    again = np.array([v for _, v in sorted(gt.pagerank(g, 0.85, 20).items())])
+    assert np.array_equal(again, blocked)  # deterministic run to run
