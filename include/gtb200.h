@@ -111,6 +111,18 @@ GT_API int gt_graph_device_views(const gt_graph* g, const int64_t** d_ids,
                           const int64_t** d_out_off, const int32_t** d_out_adj,
                           const int64_t** d_in_off, const int32_t** d_in_adj);
 
+/* Per-node lookups without exporting the CSR (Graph.record / has_node /
+ * has_edge, graphs.py:62-88, 148-167; DeviceGraph uses them until a full
+ * host copy exists). gt_graph_find: dense index of each of k node ids (-1
+ * if absent). gt_graph_row: the out (in_side = 0) or in (1) neighbours of
+ * dense index `index` as original ids, ascending; *h_len = row length, the
+ * row is copied when h_nbrs != NULL and cap >= length. gt_graph_has_edge:
+ * *h_result = 1 if the directed edge src_id -> dst_id exists. */
+GT_API int gt_graph_find(const gt_graph* g, const int64_t* h_ids, int64_t k, int64_t* h_index);
+GT_API int gt_graph_row(const gt_graph* g, int64_t index, int in_side, int64_t* h_nbrs,
+                        int64_t cap, int64_t* h_len);
+GT_API int gt_graph_has_edge(const gt_graph* g, int64_t src_id, int64_t dst_id, int* h_result);
+
 GT_API void gt_graph_free(gt_graph* g);
 
 /* ---- graph -> table (convert.py:178-217) ----------- */

@@ -39,6 +39,10 @@ SIGNATURES = {
                                              ctypes.POINTER(_VP), ctypes.POINTER(_VP),
                                              ctypes.POINTER(_VP)]),
     "gt_graph_free": (None, [_VP]),
+    "gt_graph_find": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, _VP]),
+    "gt_graph_row": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int, _VP, ctypes.c_int64, _I64P]),
+    "gt_graph_has_edge": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int64,
+                                         ctypes.POINTER(ctypes.c_int)]),
     "gt_pagerank": (ctypes.c_int, [_VP, ctypes.c_double, ctypes.c_int, _VP, ctypes.c_int]),
     "gt_graph_edge_table": (ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int]),
     "gt_tsv_count_lines": (ctypes.c_int, [_VP, ctypes.c_int64, _I64P]),
@@ -234,6 +238,35 @@ def graph_device_views(handle: int):
     check(load().gt_graph_device_views(handle, *[ctypes.byref(p) for p in ptrs]),
           "gt_graph_device_views")
     return [int(p.value or 0) for p in ptrs]
+
+
+def graph_find(handle: int, node_ids) -> np.ndarray:
+    """Dense index of each node id (-1 when absent), searched on the device."""
+    lib = ensure_init()
+    q = np.ascontiguousarray(node_ids, dtype=np.int64)
+    out = np.empty(q.shape[0], dtype=np.int64)
+    check(lib.gt_graph_find(handle, _ptr(q), q.shape[0], _ptr(out)), "gt_graph_find")
+    return out
+
+
+def graph_row(handle: int, index: int, in_side: bool) -> np.ndarray:
+    """One adjacency row (original ids) copied from the device."""
+    lib = ensure_init()
+    n = ctypes.c_int64()
+    check(lib.gt_graph_row(handle, int(index), int(in_side), None, 0, ctypes.byref(n)),
+          "gt_graph_row")
+    out = np.empty(n.value, dtype=np.int64)
+    if n.value:
+        check(lib.gt_graph_row(handle, int(index), int(in_side), _ptr(out), n.value,
+                               ctypes.byref(n)), "gt_graph_row")
+    return out
+
+
+def graph_has_edge(handle: int, src: int, dst: int) -> bool:
+    lib = ensure_init()
+    r = ctypes.c_int()
+    check(lib.gt_graph_has_edge(handle, int(src), int(dst), ctypes.byref(r)), "gt_graph_has_edge")
+    return bool(r.value)
 
 
 def graph_free(handle: int):

@@ -272,6 +272,49 @@ __global__ void __launch_bounds__(256) gather_ids_kernel(const int32_t* __restri
     out[i] = ids[adj[i]];
 }
 
+
+// ---- per-node lookups (Graph.record / has_node / has_edge, graphs.py:62-88,
+// 148-167) without exporting the CSR: binary searches on the device, one
+// row gathered and copied back.
+__device__ __forceinline__ int64_t gl_find(const int64_t* __restrict__ ids, int64_t n, int64_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t m = (lo + hi) >> 1;
+    if (ids[m] < x) lo = m + 1;
+    else hi = m;
+  }
+  return (lo < n && ids[lo] == x) ? lo : -1;
+}
+
+__global__ void gl_find_kernel(const int64_t* __restrict__ ids, int64_t n,
+                               const int64_t* __restrict__ q, int64_t k, int64_t* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < k) out[i] = gl_find(ids, n, q[i]);
+}
+
+__global__ void gl_has_edge_kernel(const int64_t* __restrict__ ids, int64_t n,
+                                   const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
+                                   int64_t src, int64_t dst, int64_t* __restrict__ out) {
+  const int64_t a = gl_find(ids, n, src), b = gl_find(ids, n, dst);
+  int64_t r = 0;
+  if (a >= 0 && b >= 0) {
+    int64_t lo = off[a], hi = off[a + 1];
+    while (lo < hi) {
+      const int64_t m = (lo + hi) >> 1;
+      if (adj[m] < int32_t(b)) lo = m + 1;
+      else hi = m;
+    }
+    r = (lo < off[a + 1] && adj[lo] == int32_t(b)) ? 1 : 0;
+  }
+  out[0] = r;
+}
+
+__global__ void gl_row_kernel(const int64_t* __restrict__ ids, const int32_t* __restrict__ adj,
+                              int64_t begin, int64_t len, int64_t* __restrict__ out) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += stride)
+    out[i] = ids[adj[begin + i]];
+}
 }  // namespace gtd
 
 namespace gt {
@@ -576,6 +619,55 @@ int gt_graph_device_views(const gt_graph* g, const int64_t** d_ids, const int64_
   if (d_out_adj) *d_out_adj = g->out_adj;
   if (d_in_off) *d_in_off = g->in_off;
   if (d_in_adj) *d_in_adj = g->in_adj;
+  GT_API_END
+}
+
+int gt_graph_find(const gt_graph* g, const int64_t* h_ids, int64_t k, int64_t* h_index) {
+  GT_API_BEGIN
+  require_init();
+  if (!g || k < 0 || (k > 0 && (!h_ids || !h_index))) fail(GT_EINVAL, "bad arguments");
+  if (k == 0) return GT_OK;
+  int64_t* d = ws_n<int64_t>(WS_SMALL, size_t(2 * k) + 16);
+  h2d(d, h_ids, size_t(k) * 8);
+  GT_LAUNCH(gtd::gl_find_kernel, ceil_div(k, 256), 256, 0, g->ids, g->n, d, k, d + k);
+  d2h(h_index, d + k, size_t(k) * 8);
+  sync();
+  GT_API_END
+}
+
+int gt_graph_row(const gt_graph* g, int64_t index, int in_side, int64_t* h_nbrs, int64_t cap,
+                 int64_t* h_len) {
+  GT_API_BEGIN
+  require_init();
+  if (!g || !h_len || index < 0 || index >= g->n) fail(GT_EINVAL, "bad arguments");
+  const int64_t* off = in_side ? g->in_off : g->out_off;
+  const int32_t* adj = in_side ? g->in_adj : g->out_adj;
+  int64_t be[2];
+  d2h(be, off + index, 16);
+  sync();
+  const int64_t len = be[1] - be[0];
+  *h_len = len;
+  if (!h_nbrs || cap < len || len == 0) return GT_OK;
+  int64_t* d = ws_n<int64_t>(WS_TMP4, size_t(len));
+  GT_LAUNCH(gtd::gl_row_kernel, std::max(1, std::min(ceil_div(len, 256), 4 * ctx().sm_count)), 256,
+            0, g->ids, adj, be[0], len, d);
+  d2h(h_nbrs, d, size_t(len) * 8);
+  sync();
+  GT_API_END
+}
+
+int gt_graph_has_edge(const gt_graph* g, int64_t src_id, int64_t dst_id, int* h_result) {
+  GT_API_BEGIN
+  require_init();
+  if (!g || !h_result) fail(GT_EINVAL, "bad arguments");
+  int64_t* d = ws_n<int64_t>(WS_SMALL, 16);
+  if (g->n == 0) { *h_result = 0; return GT_OK; }
+  GT_LAUNCH(gtd::gl_has_edge_kernel, 1, 1, 0, g->ids, g->n, g->out_off, g->out_adj, src_id, dst_id,
+            d + 15);
+  int64_t r = 0;
+  d2h(&r, d + 15, 8);
+  sync();
+  *h_result = int(r);
   GT_API_END
 }
 

@@ -269,6 +269,7 @@ class DeviceGraph(_GraphReadAPI):
         self._handle = handle
         self._n, self._e = _native.graph_sizes(handle)
         self._host: _HostCSR | None = None
+        self._ids: np.ndarray | None = None  # ids alone, for node_ids()
         self._graph: Graph | None = None  # set once mutated
         self._finalizer = weakref.finalize(self, _native.graph_free, handle)
 
@@ -305,15 +306,39 @@ class DeviceGraph(_GraphReadAPI):
     def node_ids(self) -> list[int]:
         if self._graph is not None:
             return self._graph.node_ids()
-        return self.csr().ids.tolist()
+        if self._host is not None:
+            return self._host.ids.tolist()
+        if self._ids is None:  # ids only (8 B per node), not the whole CSR
+            ids = np.empty(self._n, dtype=np.int64)
+            _native.check(_native.load().gt_graph_export(self.handle, _native._ptr(ids), None, None,
+                                                         None, None), "gt_graph_export")
+            self._ids = _frozen(ids)
+        return self._ids.tolist()
+
+    @staticmethod
+    def _as_id(node_id):
+        try:
+            x = int(node_id)
+        except (TypeError, ValueError, OverflowError):
+            return None
+        if x != node_id or not (-(1 << 63) <= x < (1 << 63)):
+            return None
+        return x
 
     def _index(self, node_id) -> int:
-        ids = self.csr().ids
-        try:
-            pos = int(np.searchsorted(ids, node_id))
-        except (TypeError, OverflowError):
-            pos = ids.shape[0]
-        if pos >= ids.shape[0] or ids[pos] != node_id:
+        if self._host is not None:
+            ids = self._host.ids
+            try:
+                pos = int(np.searchsorted(ids, node_id))
+            except (TypeError, OverflowError):
+                pos = ids.shape[0]
+            if pos >= ids.shape[0] or ids[pos] != node_id:
+                raise UnknownNodeError(f"node {node_id} not in graph")
+            return pos
+        # no host copy: binary search on the device (no O(E) transfer)
+        x = self._as_id(node_id)
+        pos = -1 if x is None else int(_native.graph_find(self.handle, [x])[0])
+        if pos < 0:
             raise UnknownNodeError(f"node {node_id} not in graph")
         return pos
 
@@ -330,9 +355,21 @@ class DeviceGraph(_GraphReadAPI):
         if self._graph is not None:
             return self._graph.record(node_id)
         i = self._index(node_id)
-        h = self.csr()
+        h = self._host
+        if h is None:  # one row each way from the device
+            return NodeRecord(int(node_id),
+                              in_nbrs=_frozen(_native.graph_row(self.handle, i, True)),
+                              out_nbrs=_frozen(_native.graph_row(self.handle, i, False)))
         return NodeRecord(int(node_id), in_nbrs=h.in_adj[h.in_off[i]:h.in_off[i + 1]],
                           out_nbrs=h.out_adj[h.out_off[i]:h.out_off[i + 1]])
+
+    def has_edge(self, src: int, dst: int) -> bool:
+        if self._graph is not None or self._host is not None:
+            return super().has_edge(src, dst)
+        a, b = self._as_id(src), self._as_id(dst)
+        if a is None or b is None:
+            return False
+        return _native.graph_has_edge(self.handle, a, b)
 
     def out_csr(self):
         if self._graph is not None:

@@ -302,3 +302,43 @@ def test_c4_full_size_properties():
         _native.check(lib.gt_triangles_part(g.handle, p, 4, ctypes.byref(c)), "gt_triangles_part")
         parts += c.value
     assert parts == total  # exact value: tests/test_large_gpu.py (oracle on a slice)
+
+
+def test_per_node_lookups_stay_on_the_device():
+    """record / has_node / has_edge / neighbors answered by device binary
+    searches + one copied row (no O(E) export): the same answers as the host
+    copy (graphs.py:62-88, 148-167), on a graph with hubs and negative ids."""
+    import time
+
+    src, dst = rmat_edges(14, 200_000, seed=5, permute=True)
+    src = src - 1000
+    g = gt.table_to_graph(gt.edge_table(src, dst).to_device(), SPEC)
+    rng = np.random.default_rng(0)
+    ids = np.unique(np.concatenate([src, dst]))
+    probe = np.concatenate([rng.choice(ids, 40), [ids[0], ids[-1]], [-5000, 10**12]])
+    got = {}
+    for x in probe.tolist():
+        got[x] = (g.has_node(x), g.record(x) if g.has_node(x) else None)
+    u = rng.choice(ids, 60)
+    v = rng.choice(ids, 60)
+    edges = [g.has_edge(a, b) for a, b in zip(u.tolist(), v.tolist())]
+    real = [g.has_edge(int(a), int(b)) for a, b in zip(src[:30].tolist(), dst[:30].tolist())]
+    assert all(real)
+    assert g._host is None  # nothing exported so far
+    t0 = time.perf_counter()
+    for a, b in zip(src[:200].tolist(), dst[:200].tolist()):
+        g.has_edge(a, b)
+    assert (time.perf_counter() - t0) / 200 < 1e-3  # < 1 ms per lookup
+    h = g.csr()  # host copy, the reference layout
+    for x, (present, rec) in got.items():
+        i = int(np.searchsorted(h.ids, x))
+        assert present == (i < h.ids.shape[0] and h.ids[i] == x)
+        if present:
+            assert np.array_equal(rec.out_nbrs, h.out_adj[h.out_off[i]:h.out_off[i + 1]])
+            assert np.array_equal(rec.in_nbrs, h.in_adj[h.in_off[i]:h.in_off[i + 1]])
+            assert not rec.out_nbrs.flags.writeable
+    for a, b, e in zip(u.tolist(), v.tolist(), edges):
+        i = int(np.searchsorted(h.ids, a))
+        row = h.out_adj[h.out_off[i]:h.out_off[i + 1]]
+        assert e == bool(np.isin(b, row))
+    assert g.node_ids() == h.ids.tolist()

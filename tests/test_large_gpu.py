@@ -126,6 +126,23 @@ def _check_pagerank(h):
     assert abs(float(got.sum()) - 1.0) < 1e-9
 
 
+def _check_lookups(h):
+    """has_edge / record on the 1.47 B-edge graph without a host export:
+    < 1 ms per lookup."""
+    import time
+
+    g = h["g"]
+    src, dst = h["src"], h["dst"]
+    t0 = time.perf_counter()
+    for a, b in zip(src[:100].tolist(), dst[:100].tolist()):
+        assert g.has_edge(a, b)
+    dt = (time.perf_counter() - t0) / 100
+    assert dt < 1e-3, f"has_edge {dt * 1e3:.2f} ms"
+    rec = g.record(int(src[0]))
+    assert int(dst[0]) in set(rec.out_nbrs.tolist())
+    assert g._host is None
+
+
 @pytest.fixture(scope="module")
 def c4():
     h = _build("c4")
@@ -135,6 +152,7 @@ def c4():
 
 def test_c4_node_set_and_rows(c4):
     _check_node_set(c4)
+    _check_lookups(c4)
     for side in (0, 1):
         _check_rows(c4, side, _sample(c4, side, seed=side))
 
