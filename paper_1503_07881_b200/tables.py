@@ -293,6 +293,31 @@ def load_tsv(path, schema: Schema, device=None) -> ColumnTable:
     return _load_tsv_host(path, schema)
 
 
+def load_tsv_frontend(path, schema: Schema) -> ColumnTable:
+    """LoadTableTSV's ingest (front-end __init__.py:126-128 -> tables.py:246-284):
+    all-int schemas of ASCII text are parsed on the GPU into HBM-resident
+    columns (the hot path's input: ToGraph, Select, Join read them in place);
+    str / float columns and non-ASCII text keep the host parser, which is the
+    reference's own semantics for those types (Python int()/float() on
+    Unicode, string pools). Values and errors are identical either way
+    (tests/test_tsv_gpu.py, goldens of the real reference in tsv.npz)."""
+    from . import _native
+
+    if all(t == INT for _, t in schema.columns) and len(schema.columns) <= 16:
+        try:
+            import torch
+
+            cuda = torch.cuda.is_available()
+        except Exception:  # pragma: no cover - torch is a hard dependency
+            cuda = False
+        if cuda:
+            try:
+                return _load_tsv_device(path, schema, f"cuda:{_native.device_ordinal()}")
+            except TypeMismatchError:
+                pass  # non-ASCII text: Python int() semantics on Unicode digits
+    return _load_tsv_host(path, schema)
+
+
 def _line_bounds(data: np.ndarray, k: int):
     """Byte range of the k-th line (0-based) under universal newlines."""
     nl = data == 10
