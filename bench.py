@@ -71,6 +71,11 @@ def parse_args():
     p.add_argument("--tsv-rows", type=int, default=4_000_000)
     p.add_argument("--sharded", action="store_true",
                    help="use the multi-GPU (distributed.py) pipeline even on one GPU")
+    p.add_argument("--dry-run", action="store_true",
+                   help="harness check on CPU: gloo ranks, the CPU restatement of the per-rank "
+                        "primitives (tests/dist_cpu_ops.py), a small prefix of the config's "
+                        "table; prints the JSON line shape with dry_run set (not a measurement)")
+    p.add_argument("--dry-run-rows", type=int, default=200_000)
     return p.parse_args()
 
 
@@ -94,11 +99,12 @@ def maybe_reexec(args):
         return
     import socket
 
-    import torch
+    if not args.dry_run:
+        import torch
 
-    visible = torch.cuda.device_count()
-    if visible < args.gpus:
-        sys.exit(f"bench.py: --gpus {args.gpus} but only {visible} CUDA device(s) visible")
+        visible = torch.cuda.device_count()
+        if visible < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but only {visible} CUDA device(s) visible")
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
@@ -896,9 +902,72 @@ def ncu_traffic(config, phase):
             "source": entry["source"]}
 
 
+def dry_run_arm(args):
+    """The multi-rank harness on CPU (gloo): strong-scaling shards of the
+    config's table (a prefix of it), the sharded pipeline of distributed.py
+    over the CPU restatement of its primitives, max-over-ranks timing, one
+    JSON line from rank 0. Checks the launch plumbing (torchrun re-exec,
+    rank/world, shard ranges, collectives), never a performance number."""
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, str(REPO / "tests"))
+    from dist_cpu_ops import CpuOps
+
+    from paper_1503_07881_b200 import distributed as D
+    from paper_1503_07881_b200.synth import spec_edges
+
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    else:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29534")
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    spec = spec_for(args.config)
+    rows = min(args.dry_run_rows, spec.rows)
+    lo, hi = shard_range(rank, world, rows)
+    src_all, dst_all = spec_edges(spec, rows)
+    src = torch.from_numpy(src_all[lo:hi].copy())
+    dst = torch.from_numpy(dst_all[lo:hi].copy())
+    ops = CpuOps()
+    state = {}
+
+    def step():
+        sg = D.build_csr(src, dst, ops=ops)
+        D.pagerank(sg, 0.85, args.iterations, ops=ops)
+        tc = D.triangle_count(sg, ops=ops) if has_tc(spec) else None
+        state.update(n=sg.n, e=sg.e, tc=tc)
+
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dist.barrier()
+    t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) * 1e3 / max(args.steps, 1)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": rows / (ms / 1e3), "unit": "rows/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "int64+f64", "data": "synthetic",
+            "dry_run": "gloo ranks on CPU with tests/dist_cpu_ops.py: harness check only",
+            "config": config_dict(args, spec, world) | {"dry_run_rows": rows},
+            "graph": {"nodes": state["n"], "edges": state["e"], "triangles": state["tc"]},
+            "shard": [shard_range(r, world, rows) for r in range(world)]}), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse_args()
     maybe_reexec(args)
+    if args.dry_run:
+        return dry_run_arm(args)
     if args.impl == "reference":
         return reference_arm(args)
     return ours_arm(args)

@@ -323,6 +323,12 @@ GT_API int gt_csr_from_keys(const uint64_t* d_sorted, int64_t m, int kbits, int6
 GT_API int gt_graph_from_csr(int64_t n, int64_t e, const int64_t* d_ids, const int64_t* d_out_off,
                              const int32_t* d_out_adj, const int64_t* d_in_off,
                              const int32_t* d_in_adj, gt_graph** out);
+/* Multi-GPU PageRank exchange layout: d_out[i] = r*m + (d_in[i] - bounds[r])
+ * for the rank r whose dst range [bounds[r], bounds[r+1]) holds d_in[i]
+ * (world <= 64, h_bounds host int64[world+1]): positions in the padded
+ * buffer that all_gather_into_tensor fills with one m-sized chunk per rank. */
+GT_API int gt_remap_padded(const int32_t* d_in, int64_t e, const int64_t* h_bounds, int world,
+                           int64_t m, int32_t* d_out);
 /* d_inv[v] = 1/(off[v+1]-off[v]), 0 for an empty row. */
 GT_API int gt_inv_degree(const int64_t* d_off, int64_t rows, double* d_inv);
 /* PageRank start from the full 1/outdeg vector: contrib = inv/N and the

@@ -87,6 +87,8 @@ SIGNATURES = {
     "gt_graph_from_csr": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, _VP, _VP, _VP, _VP, _VP,
                                          ctypes.POINTER(_VP)]),
     "gt_inv_degree": (ctypes.c_int, [_VP, ctypes.c_int64, _VP]),
+    "gt_remap_padded": (ctypes.c_int, [_VP, ctypes.c_int64, _VP, ctypes.c_int, ctypes.c_int64,
+                                       _VP]),
     "gt_pagerank_init": (ctypes.c_int, [_VP, ctypes.c_int64, _VP, _VP]),
     "gt_pagerank_step": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                         _VP, _VP, _VP, ctypes.c_double, ctypes.c_int, _VP, _VP,

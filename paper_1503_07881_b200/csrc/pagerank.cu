@@ -656,6 +656,26 @@ __global__ void __launch_bounds__(256) pr_blk_finalize_kernel(
   grid_reduce_last(dang, partials, ticket, dangling_next);
 }
 
+// Multi-GPU PageRank exchange layout: node v owned by rank r (bounds[r] <= v
+// < bounds[r+1]) sits at padded position r*m + (v - bounds[r]) of the
+// all-gathered contribution buffer (one equal-size chunk per rank).
+__global__ void __launch_bounds__(256) pr_remap_padded_kernel(const int32_t* __restrict__ in,
+                                                              int64_t e,
+                                                              const int64_t* __restrict__ bounds,
+                                                              int world, int64_t m,
+                                                              int32_t* __restrict__ out) {
+  __shared__ int64_t sb[65];
+  for (int i = threadIdx.x; i <= world && i < 65; i += blockDim.x) sb[i] = bounds[i];
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < e; i += stride) {
+    const int64_t v = in[i];
+    int r = 0;
+    while (r + 1 < world && sb[r + 1] <= v) ++r;
+    out[i] = int32_t(int64_t(r) * m + (v - sb[r]));
+  }
+}
+
 // Distributed PageRank helpers: 1/outdeg of a CSR row range, and the start
 // vector (contrib = inv/N) with its dangling mass, from a full 1/outdeg vector.
 __global__ void __launch_bounds__(256) pr_inv_degree_kernel(const int64_t* __restrict__ off,
@@ -979,6 +999,22 @@ static void pr_step_impl(const int64_t* in_off, const int32_t* in_adj, int64_t r
 }  // namespace gt
 
 extern "C" {
+
+int gt_remap_padded(const int32_t* d_in, int64_t e, const int64_t* h_bounds, int world,
+                    int64_t m, int32_t* d_out) {
+  GT_API_BEGIN
+  require_init();
+  if (world < 1 || world > 64 || e < 0 || !h_bounds) fail(GT_EINVAL, "bad arguments");
+  if (int64_t(world) * m >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "padded layout >= 2^31");
+  if (e == 0) return GT_OK;
+  int64_t* d_b = ws_n<int64_t>(WS_SMALL, 80);
+  h2d(d_b, h_bounds, size_t(world + 1) * 8);
+  GT_LAUNCH(gtd::pr_remap_padded_kernel,
+            static_cast<int>(std::min<int64_t>(ceil_div64(e, 1024), 8LL * ctx().sm_count)), 256, 0,
+            d_in, e, d_b, world, m, d_out);
+  sync();
+  GT_API_END
+}
 
 int gt_inv_degree(const int64_t* d_off, int64_t rows, double* d_inv) {
   GT_API_BEGIN

@@ -183,6 +183,15 @@ class NativeOps:
         self._ck(self.lib.gt_inv_degree(off.data_ptr(), rows, inv.data_ptr()), "gt_inv_degree")
         return inv[:rows]
 
+    def remap_padded(self, in_adj, bounds, m):
+        self._pre()
+        b = np.ascontiguousarray(np.asarray(bounds, dtype=np.int64))
+        out = torch.empty_like(in_adj)
+        self._ck(self.lib.gt_remap_padded(in_adj.data_ptr(), in_adj.numel(), b.ctypes.data,
+                                          len(bounds) - 1, int(m), out.data_ptr()),
+                 "gt_remap_padded")
+        return out
+
     def pagerank_init(self, inv_full):
         self._pre()
         n = inv_full.numel()
@@ -219,21 +228,6 @@ class NativeOps:
 
 def _world(group):
     return dist.get_world_size(group), dist.get_rank(group)
-
-
-def _all_gather_var(t: torch.Tensor, group) -> list[torch.Tensor]:
-    """All-gather 1-D tensors of different lengths (padded exchange)."""
-    world, _ = _world(group)
-    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
-    sizes = [torch.empty_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n, group=group)
-    sizes = [int(s.item()) for s in sizes]
-    mx = max(max(sizes), 1)
-    pad = torch.zeros(mx, dtype=t.dtype, device=t.device)
-    pad[: t.numel()] = t
-    out = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(out, pad, group=group)
-    return [o[:s] for o, s in zip(out, sizes)]
 
 
 def _exchange(send: torch.Tensor, splits: np.ndarray, group) -> torch.Tensor:
@@ -365,24 +359,46 @@ def build_csr(src: torch.Tensor, dst: torch.Tensor, group=None, ops=None) -> Sha
 
 def gather_csr(sg: ShardedGraph, group=None):
     """Replicate the full CSR pair on every rank (offsets rebased)."""
-    def full(off, adj, counts):
-        offs = _all_gather_var(off[:-1], group)
-        adjs = _all_gather_var(adj, group)
-        base = np.concatenate([[0], np.cumsum(counts)])
-        parts = [o + int(b) for o, b in zip(offs, base[:-1])]
-        tail = torch.tensor([int(base[-1])], dtype=torch.int64, device=off.device)
-        return torch.cat(parts + [tail]), torch.cat(adjs)
+    world, _ = _world(group)
 
-    out_off, out_adj = full(sg.out_off, sg.out_adj, sg.out_counts)
-    in_off, in_adj = full(sg.in_off, sg.in_adj, sg.in_counts)
+    def full(off, adj, counts, bounds):
+        rows = [bounds[r + 1] - bounds[r] for r in range(world)]
+        offs = _gather_known(off[:-1], rows, group)  # sizes known everywhere
+        adjs = _gather_known(adj, list(counts), group)
+        base = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        row_base = torch.from_numpy(np.repeat(base[:-1], rows)).to(off.device)
+        tail = torch.tensor([int(base[-1])], dtype=torch.int64, device=off.device)
+        return torch.cat([offs + row_base, tail]), adjs
+
+    out_off, out_adj = full(sg.out_off, sg.out_adj, sg.out_counts, sg.out_bounds)
+    in_off, in_adj = full(sg.in_off, sg.in_adj, sg.in_counts, sg.in_bounds)
     return out_off, out_adj, in_off, in_adj
 
 
 # ---------------------------------------------------------------- PageRank --
 
+def _gather_known(t: torch.Tensor, sizes: list[int], group) -> torch.Tensor:
+    """All-gather of 1-D slices whose sizes every rank already knows (no size
+    exchange, no host syncs): one all_gather_into_tensor of m-sized chunks."""
+    world, rank = _world(group)
+    m = max(max(sizes), 1)
+    buf = torch.empty(world * m, dtype=t.dtype, device=t.device)
+    buf[rank * m: rank * m + t.numel()] = t
+    dist.all_gather_into_tensor(buf, buf[rank * m:(rank + 1) * m], group=group)
+    return torch.cat([buf[r * m: r * m + sizes[r]] for r in range(world)])
+
+
 def pagerank(sg: ShardedGraph, damping: float = 0.85, iterations: int = 10, group=None,
              ops=None) -> torch.Tensor:
-    """Scores of all nodes (id order) on every rank (algorithms.py:36-87)."""
+    """Scores of all nodes (id order) on every rank (algorithms.py:36-87).
+
+    1D dst-range partition: rank r computes the rows
+    [in_bounds[r], in_bounds[r+1]); the contribution vector lives in a padded
+    buffer of one m-sized chunk per rank, filled every iteration by ONE
+    in-place all_gather_into_tensor (the slice sizes follow from the
+    replicated bounds: no size exchange, no host round trip); the local
+    in-adjacency is remapped once to padded positions. The dangling mass is
+    one all-reduced double per iteration."""
     if not 0.0 < damping < 1.0:
         raise ValueError(f"damping must be in (0, 1), got {damping}")
     if iterations < 1:
@@ -390,20 +406,31 @@ def pagerank(sg: ShardedGraph, damping: float = 0.85, iterations: int = 10, grou
     if sg.n == 0:
         raise ValueError("pagerank needs a non-empty graph")
     ops = ops or NativeOps()
-    _, rank = _world(group)
-    inv_full = torch.cat(_all_gather_var(ops.inv_degree(sg.out_off), group))
-    contrib, dangling = ops.pagerank_init(inv_full)
+    world, rank = _world(group)
+    out_sizes = [sg.out_bounds[r + 1] - sg.out_bounds[r] for r in range(world)]
+    sizes = [sg.in_bounds[r + 1] - sg.in_bounds[r] for r in range(world)]
+    m = max(max(sizes), 1)
+    inv_full = _gather_known(ops.inv_degree(sg.out_off), out_sizes, group)
+    contrib0, dangling = ops.pagerank_init(inv_full)
     i_lo, i_hi = sg.in_bounds[rank], sg.in_bounds[rank + 1]
     inv_rows = inv_full[i_lo:i_hi].contiguous()
+    adj_p = ops.remap_padded(sg.in_adj, sg.in_bounds, m)
+    bufs = [torch.zeros(world * m, dtype=torch.float64, device=contrib0.device) for _ in range(2)]
+    for r in range(world):  # initial contributions in the padded layout
+        a, b = sg.in_bounds[r], sg.in_bounds[r + 1]
+        bufs[0][r * m: r * m + (b - a)] = contrib0[a:b]
+    del contrib0
     for it in range(iterations):
         last = it == iterations - 1
-        vals, part = ops.pagerank_step(sg.in_off, sg.in_adj, sg.n, contrib, inv_rows, dangling,
+        cur, nxt = bufs[it & 1], bufs[(it + 1) & 1]
+        vals, part = ops.pagerank_step(sg.in_off, adj_p, sg.n, cur, inv_rows, dangling,
                                        damping, last)
+        nxt[rank * m: rank * m + vals.numel()] = vals
+        dist.all_gather_into_tensor(nxt, nxt[rank * m:(rank + 1) * m], group=group)
         if last:
-            return torch.cat(_all_gather_var(vals, group))
+            return torch.cat([nxt[r * m: r * m + sizes[r]] for r in range(world)])
         dist.all_reduce(part, group=group)
         dangling = part
-        contrib = torch.cat(_all_gather_var(vals, group))
     raise AssertionError("unreachable")
 
 

@@ -99,6 +99,12 @@ class CpuOps:
         inv[d > 0] = 1.0 / d[d > 0]
         return torch.from_numpy(inv)
 
+    def remap_padded(self, in_adj, bounds, m):
+        v = in_adj.numpy().astype(np.int64)
+        b = np.asarray(bounds, dtype=np.int64)
+        r = np.searchsorted(b[1:-1], v, side="right")
+        return torch.from_numpy((r * m + (v - b[r])).astype(np.int32))
+
     def pagerank_init(self, inv_full):
         inv = inv_full.numpy()
         n = inv.size

@@ -1,4 +1,4 @@
-"""Multi-process path (distributed.py) on CPU: gloo, world size 2 and 3.
+"""Multi-process path (distributed.py) on CPU: gloo, world size 2, 3 and 4.
 
 Drives the real orchestration — id-range and presence all-reduces, splitter
 histograms, the two all-to-all shuffles, offset rebasing, PageRank's
@@ -132,3 +132,13 @@ def test_two_ranks_empty_table(tmp_path):
     src = np.zeros(0, dtype=np.int64)
     res = _run(tmp_path, src, src, 2)
     assert int(res["n"]) == 0 and int(res["e"]) == 0 and int(res["tc"]) == 0
+
+
+def test_four_ranks_rmat_with_hubs(tmp_path):
+    """World size 4, uneven slices: PageRank's padded all-gather layout with
+    unequal dst ranges, the shuffles, the triangle split."""
+    from paper_1503_07881_b200.synth import rmat_edges
+
+    src, dst = rmat_edges(10, 9000, seed=8, permute=True)
+    cuts = [0, 1000, 4000, 4100, src.shape[0]]
+    _check(_run(tmp_path, src, dst, 4, cuts=cuts), src, dst)
