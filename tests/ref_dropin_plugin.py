@@ -25,6 +25,10 @@ def pytest_configure(config):
         mod.pagerank = b200.pagerank
         mod.triangle_count = b200.triangle_count
     config.addinivalue_line("markers", "slow: reference marker")
+    import sys
+
+    sys.stderr.write(f"drop-in: graphtables.table_to_graph/pagerank/triangle_count -> "
+                     f"{b200.table_to_graph.__module__} (libgtb200.so)\n")
 
 
 def pytest_report_header(config):
