@@ -16,6 +16,8 @@ import numpy as np
 from .errors import CapacityError, NativeError
 
 LIB_PATH = Path(__file__).resolve().parent / "libgtb200.so"
+if os.environ.get("GT_LIB_VARIANT"):  # build-knob sweeps (scripts/sweep_*.sh) only
+    LIB_PATH = LIB_PATH.with_name(f"libgtb200_{os.environ['GT_LIB_VARIANT']}.so")
 
 GT_OK, GT_EINVAL, GT_ENOMEM, GT_ECUDA, GT_ENCCL, GT_ECAPACITY, GT_ENODEV = range(7)
 

@@ -1307,6 +1307,29 @@ static void seg_level(const uint64_t* in, uint64_t* out, const int64_t* d_seg_be
   }
 }
 
+// A non-stable partition of n keys by (key >> shift) & (2^bits - 1) into
+// digit-sorted order, digit starts given (the first pass of an LSD sort needs
+// no stability: nothing orders equal digits yet). 4.2 TB/s vs 2.4 TB/s for
+// the stable onesweep pass on B200 (scripts/ubench/ubench_r2.cu).
+void partition_pass(const uint64_t* in, uint64_t* out, int64_t n, int shift, int bits,
+                    const int64_t* d_digit_base) {
+  cudaStream_t st = ctx().stream;
+  const int nd = 1 << bits;
+  int64_t* d_seg = ws_n<int64_t>(WS_TMP3, 8);  // begin, end, tile offsets {0, tiles}
+  unsigned long long* d_cur = ws_n<unsigned long long>(WS_TMP4, size_t(nd));
+  const int64_t h_seg[4] = {0, n, 0, ceil_div64(n, PART_T)};
+  h2d(d_seg, h_seg, sizeof h_seg);
+  GT_CUDA(cudaMemcpyAsync(d_cur, d_digit_base, size_t(nd) * 8, cudaMemcpyDeviceToDevice, st));
+  const size_t smem = size_t(PART_T) * 8 + gtd::BK_MAXD * 12 + 64;
+  static const bool once = [&] {
+    set_smem(gtd::bk_seg_part_kernel<PART_KPT>, smem);
+    return true;
+  }();
+  (void)once;
+  GT_LAUNCH(gtd::bk_seg_part_kernel<PART_KPT>, ctx().sm_count * 3, 256, smem, in, out, d_seg,
+            d_seg + 1, d_seg + 2, 1, shift, nd, d_cur);
+}
+
 bool bucket_build_applies(int64_t rows, uint64_t span) {
   // GT_BUILD (read per call): the LSD sort pipeline (build.cu) is the
   // default; "bucket" forces this one, "auto" picks it for large dense

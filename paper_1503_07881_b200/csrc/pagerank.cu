@@ -44,7 +44,10 @@ namespace gtd {
 // C4 203 -> 172 ms against __ldg for all; the split point itself did not
 // matter (0 .. 2^20 within noise), while a plain no_allocate load for every
 // gather compiled to a slower schedule (C2 10.7 ms).
-constexpr int PR_HOT = 1 << 15;
+#ifndef GT_PR_HOT_LOG
+#define GT_PR_HOT_LOG 15
+#endif
+constexpr int PR_HOT = 1 << GT_PR_HOT_LOG;
 __device__ __forceinline__ double pr_gather(const double* contrib, int32_t u) {
   if (u < PR_HOT) return __ldg(contrib + u);
   double v;
@@ -64,9 +67,16 @@ __device__ __forceinline__ double pr_gather_pol(const double* contrib, int32_t u
   return v;
 }
 
+// (build-time knobs for sweeps: -DGT_PR_TILE=..., -DGT_PR_MIN_BLOCKS=...)
+#ifndef GT_PR_TILE
+#define GT_PR_TILE 2048
+#endif
+#ifndef GT_PR_MIN_BLOCKS
+#define GT_PR_MIN_BLOCKS 6
+#endif
 constexpr int PR_THREADS = 256;
-constexpr int PR_TILE = 2048;
-constexpr int PR_MIN_BLOCKS = 6;  // resident CTAs per SM the register budget is sized for
+constexpr int PR_TILE = GT_PR_TILE;
+constexpr int PR_MIN_BLOCKS = GT_PR_MIN_BLOCKS;  // resident CTAs per SM the register budget is sized for
 
 // Last-block deterministic reduction of one double per block.
 __device__ __forceinline__ void grid_reduce_last(double block_val, double* partials,

@@ -306,7 +306,7 @@ static void launch_onesweep(int bits, int nmatch, int grid, const uint64_t* src,
 }
 
 uint64_t* radix_sort(uint64_t* a, uint64_t* b, int64_t n, const SortPlan& plan, SortHist h,
-                     const char* phase) {
+                     const char* phase, bool first_unstable) {
   if (n <= 1 || plan.passes == 0) return a;
   const int64_t tiles = ceil_div64(n, RS_TILE);
   if (tiles >= (1ll << 31)) fail(GT_ECAPACITY, "radix sort: too many tiles");
@@ -323,8 +323,17 @@ uint64_t* radix_sort(uint64_t* a, uint64_t* b, int64_t n, const SortPlan& plan, 
     const char* env = getenv("GT_SORT_MATCH");
     return env ? atoi(env) : 6;
   }();
+  static const bool stable_only = [] {  // GT_SORT_STABLE_FIRST=1: onesweep for every pass
+    const char* env = getenv("GT_SORT_STABLE_FIRST");
+    return env && atoi(env);
+  }();
   for (int q = 0; q < plan.passes; ++q) {
     Phase ph(phase, 16.0 * n);
+    if (q == 0 && first_unstable && !stable_only) {
+      partition_pass(src, dst, n, plan.shift[q], plan.bits[q], h.digit_base + q * 256);
+      std::swap(src, dst);
+      continue;
+    }
     const uint32_t epoch = next_epoch();
     launch_onesweep(plan.bits[q], nmatch, static_cast<int>(tiles), src, dst, n, plan.shift[q],
                     h.digit_base + q * 256, status, counters + q, epoch);

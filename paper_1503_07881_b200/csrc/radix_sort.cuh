@@ -44,8 +44,14 @@ void sort_histogram(const uint64_t* keys, int64_t n, const SortPlan& plan, SortH
 // Sort n keys (in `a`) by `plan`; `b` is scratch of the same size. The
 // histogram `h` must already hold the digit counts of the keys. Returns the
 // buffer that holds the sorted result (a or b).
+// first_unstable: the caller's input order does not matter (full-key sorts),
+// so the first pass may be a non-stable partition (partition_pass).
 uint64_t* radix_sort(uint64_t* a, uint64_t* b, int64_t n, const SortPlan& plan, SortHist h,
-                     const char* phase);
+                     const char* phase, bool first_unstable = false);
+
+// bucket_build.cu
+void partition_pass(const uint64_t* in, uint64_t* out, int64_t n, int shift, int bits,
+                    const int64_t* d_digit_base);
 
 }  // namespace gt
 
