@@ -782,13 +782,16 @@ def ours_arm(args):
             def e2e_step():
                 # pipelined ingest: this step's table was copied (pinned host ->
                 # HBM, side stream) while the previous step computed; the next
-                # step's copy is issued now and overlaps this step's PageRank
-                # and triangle count
+                # step's copy is issued first, so that it overlaps this step's
+                # build and PageRank: the copy engine's HBM writes flush L2, and
+                # the triangle count (whose suffix reads live in L2) measured
+                # 824 ms instead of 680 when the copy ran under it (e2e 1178 vs
+                # 1036 ms per C4 step, scripts/probe_e2e.py)
                 cur = pipe["next"] if pipe["next"] is not None else host_table.prefetch()
-                g = gt.table_to_graph(cur, edge_spec)
-                del cur
                 if not os.environ.get("BENCH_E2E_SERIAL"):
                     pipe["next"] = host_table.prefetch()
+                g = gt.table_to_graph(cur, edge_spec)
+                del cur
                 # scores stay in HBM until the count is done, then one D2H read:
                 # a read issued while the next table's H2D copy is in flight
                 # waited for that copy (C4: +410 ms), one after the count does not
