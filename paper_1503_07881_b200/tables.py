@@ -192,11 +192,12 @@ class ColumnTable:
         when a call first uses the table (``_await_ready``), so a copy issued
         while the library is busy overlaps that work (pipelined ingest of a
         stream of tables). Host columns should be pinned for the copy to be
-        asynchronous; str codes travel as int64, floats as float64. A
-        device->host read the library issues while the copy is in flight (a
-        size, a counter) waits for the copy: measured on B200, the two
-        directions do not overlap here, so long copies should overlap
-        kernels, not reads."""
+        asynchronous; str codes travel as int64, floats as float64. The copy
+        engine's writes go through L2 and evict what kernels running meanwhile
+        keep there: measured on B200 at C4, issuing the next table's copy at
+        the start of a step (under the build and PageRank) costs ~1 %, issuing
+        it under the triangle count ~20 % of the count
+        (scripts/probe_e2e.py, profiles/r2_e2e_probe.txt)."""
         import torch
 
         from . import _native
