@@ -305,6 +305,13 @@ GT_API int gt_pack_keys(const int64_t* d_src, const int64_t* d_dst, int64_t rows
  * (*result_in_tmp = 0) or d_tmp (1). Stable. */
 GT_API int gt_sort_keys(uint64_t* d_keys, uint64_t* d_tmp, int64_t n, int lo_bit, int hi_bit,
                         int* result_in_tmp);
+/* Merge nruns sorted runs [h_run_off[r], h_run_off[r+1]) of d_keys into one
+ * ascending sequence (earlier run first on ties); h_run_off is a HOST array of
+ * nruns+1 offsets from 0 to n. The result is in d_keys (*result_in_tmp = 0) or
+ * d_tmp (1). Replaces the re-sort of the received sample-sort buckets
+ * (parallel.py:52-93) on the receive side of the sharded build. */
+GT_API int gt_merge_runs(uint64_t* d_keys, uint64_t* d_tmp, int64_t n, const int64_t* h_run_off,
+                         int nruns, int* result_in_tmp);
 /* Drop adjacent duplicates of sorted keys (convert.py:76-80); *m = kept. */
 GT_API int gt_unique_keys(const uint64_t* d_in, int64_t n, uint64_t* d_out, int64_t* m);
 /* d_counts[b] = #{i : min(keys[i] >> shift, nbuckets-1) == b}, nbuckets <= 4096. */

@@ -80,6 +80,8 @@ SIGNATURES = {
     "gt_sort_keys": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                     ctypes.POINTER(ctypes.c_int)]),
     "gt_unique_keys": (ctypes.c_int, [_VP, ctypes.c_int64, _VP, _I64P]),
+    "gt_merge_runs": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, _VP, ctypes.c_int,
+                                     ctypes.POINTER(ctypes.c_int)]),
     "gt_key_bucket_counts": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                             _VP]),
     "gt_key_lower_bounds": (ctypes.c_int, [_VP, ctypes.c_int64, _VP, ctypes.c_int, _VP]),

@@ -120,6 +120,21 @@ class NativeOps:
                                        hi_bit, ctypes.byref(which)), "gt_sort_keys")
         return tmp if which.value else keys
 
+    def merge_runs(self, keys, run_sizes):
+        """Merge consecutive sorted runs of the given sizes (gt_merge_runs)."""
+        import ctypes
+
+        keys = keys.contiguous().clone()  # torch-stream copy: ordered before the merge by _pre
+        tmp = torch.empty_like(keys)
+        off = np.concatenate([[0], np.cumsum(np.asarray(run_sizes, dtype=np.int64))])
+        off = np.ascontiguousarray(off, dtype=np.int64)
+        self._pre()
+        which = ctypes.c_int()
+        self._ck(self.lib.gt_merge_runs(keys.data_ptr(), tmp.data_ptr(), keys.numel(),
+                                        off.ctypes.data, len(run_sizes), ctypes.byref(which)),
+                 "gt_merge_runs")
+        return tmp if which.value else keys
+
     def unique_keys(self, keys):
         import ctypes
 
@@ -230,8 +245,9 @@ def _world(group):
     return dist.get_world_size(group), dist.get_rank(group)
 
 
-def _exchange(send: torch.Tensor, splits: np.ndarray, group) -> torch.Tensor:
-    """all-to-all with uneven splits: part r of `send` goes to rank r."""
+def _exchange(send: torch.Tensor, splits: np.ndarray, group):
+    """all-to-all with uneven splits: part r of `send` goes to rank r.
+    Returns the received keys (source-rank order) and the per-source sizes."""
     world, _ = _world(group)
     send_counts = torch.tensor(np.diff(splits), dtype=torch.int64, device=send.device)
     recv_counts = torch.empty_like(send_counts)
@@ -241,7 +257,7 @@ def _exchange(send: torch.Tensor, splits: np.ndarray, group) -> torch.Tensor:
     out = torch.empty(sum(rc), dtype=send.dtype, device=send.device)
     dist.all_to_all_single(out, send.contiguous(), output_split_sizes=rc, input_split_sizes=sc,
                            group=group)
-    return out
+    return out, rc
 
 
 def _range_bounds(counts: np.ndarray, world: int, rows: int, bucket_rows: int) -> list[int]:
@@ -319,15 +335,16 @@ def build_csr(src: torch.Tensor, dst: torch.Tensor, group=None, ops=None) -> Sha
     kbits = _bits_for(n)
     sb, bucket_rows = _split_plan(n, kbits)
 
-    # out-CSR: local sort + dedupe, sample sort by src range, sort + dedupe
+    # out-CSR: local sort + dedupe, sample sort by src range, merge + dedupe
     keys = ops.pack_keys(src, dst, lo, words, kbits)
     del words
     keys = ops.unique_keys(ops.sort_keys(keys, 0, 2 * kbits))
     counts = ops.bucket_counts(keys, 2 * kbits - sb, 1 << sb)
     dist.all_reduce(counts, group=group)
     out_bounds = _range_bounds(counts.cpu().numpy(), world, n, bucket_rows)
-    mine = _shuffle_by_rows(keys, kbits, out_bounds, ops, group)
-    mine = ops.unique_keys(ops.sort_keys(mine, 0, 2 * kbits))
+    # the received runs (one per source rank) are each sorted: merge them
+    mine, sizes = _shuffle_by_rows(keys, kbits, out_bounds, ops, group)
+    mine = ops.unique_keys(ops.merge_runs(mine, sizes))
     o_lo, o_hi = out_bounds[rank], out_bounds[rank + 1]
     out_off, out_adj = ops.csr_from_keys(mine, kbits, o_lo, o_hi - o_lo)
 
@@ -339,12 +356,11 @@ def build_csr(src: torch.Tensor, dst: torch.Tensor, group=None, ops=None) -> Sha
     counts = ops.bucket_counts(ikeys, 2 * kbits - sb, 1 << sb)
     dist.all_reduce(counts, group=group)
     in_bounds = _range_bounds(counts.cpu().numpy(), world, n, bucket_rows)
-    theirs = _shuffle_by_rows(ikeys, kbits, in_bounds, ops, group)
+    theirs, sizes = _shuffle_by_rows(ikeys, kbits, in_bounds, ops, group)
     del ikeys
-    # the received runs arrive in source-rank order, each sorted by (dst, src),
-    # and rank r's sources all lie below rank r+1's (out-CSR ranges): a stable
-    # sort over the dst bits alone gives (dst, src) order
-    theirs = ops.sort_keys(theirs, kbits, 2 * kbits)
+    # the received runs arrive in source-rank order, each sorted by the whole
+    # (dst, src) key: merging them gives (dst, src) order
+    theirs = ops.merge_runs(theirs, sizes)
     i_lo, i_hi = in_bounds[rank], in_bounds[rank + 1]
     in_off, in_adj = ops.csr_from_keys(theirs, kbits, i_lo, i_hi - i_lo)
 

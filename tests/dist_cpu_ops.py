@@ -61,6 +61,15 @@ class CpuOps:
         digit = (k >> np.uint64(lo_bit)) & np.uint64((1 << (hi_bit - lo_bit)) - 1)
         return _t64(k[np.argsort(digit, kind="stable")])
 
+    def merge_runs(self, keys, run_sizes):
+        k = _u64(keys)
+        off = np.concatenate([[0], np.cumsum(np.asarray(run_sizes, dtype=np.int64))])
+        assert off[-1] == k.size
+        for r in range(len(run_sizes)):  # precondition of gt_merge_runs
+            seg = k[off[r]:off[r + 1]]
+            assert np.all(seg[1:] >= seg[:-1]), "merge_runs: run not sorted"
+        return _t64(np.sort(k, kind="stable"))
+
     def unique_keys(self, keys):
         k = _u64(keys)
         if k.size == 0:

@@ -45,6 +45,73 @@ def test_sort_unique_bounds_match_cpu(native, n, bits, lo, hi):
                            cpu.bucket_counts(want, sh, 1 << min(12, bits)))
 
 
+def _runs_by_dst_then_src(rng, nruns, kbits, per_run):
+    """Runs as the in-CSR shuffle delivers them: run r holds edges whose src
+    lie in [r*w, (r+1)*w) (rank r's out-CSR rows), each run sorted by
+    (dst, src), keys (dst << kbits) | src."""
+    w = (1 << kbits) // nruns
+    runs, sizes = [], []
+    for r in range(nruns):
+        m = int(per_run[r])
+        src = rng.integers(r * w, (r + 1) * w, size=m).astype(np.uint64)
+        dst = rng.integers(0, 1 << kbits, size=m).astype(np.uint64)
+        k = np.unique((dst << np.uint64(kbits)) | src)
+        runs.append(k)
+        sizes.append(k.size)
+    return torch.from_numpy(np.concatenate(runs).view(np.int64).copy()), sizes
+
+
+@pytest.mark.parametrize("nruns,kbits,seed", [(2, 12, 1), (3, 17, 2), (4, 20, 3), (8, 22, 4)])
+def test_sort_dst_bits_over_concatenated_runs(native, nruns, kbits, seed):
+    """The in-CSR receive side before gt_merge_runs: a stable sort over the
+    dst bits [kbits, 2*kbits) of >= 2 concatenated (dst, src)-sorted runs with
+    disjoint ascending src ranges equals the full sort over (0, 2*kbits)."""
+    rng = np.random.default_rng(seed)
+    keys, _ = _runs_by_dst_then_src(rng, nruns, kbits, rng.integers(1000, 60000, nruns))
+    got = native.sort_keys(keys.cuda(), kbits, 2 * kbits).cpu()
+    want = native.sort_keys(keys.cuda(), 0, 2 * kbits).cpu()
+    assert torch.equal(got, want)
+    assert np.array_equal(got.numpy().view(np.uint64), np.sort(keys.numpy().view(np.uint64)))
+
+
+@pytest.mark.parametrize("sizes", [[0], [1], [5, 0], [0, 7], [2048, 2048], [1, 2047, 4096, 3],
+                                   [100_000, 3, 250_000], [0, 0, 0, 0],
+                                   [30_000] * 8, [70_001, 0, 12, 9_999, 400_000, 1, 2, 65_536]])
+def test_merge_runs_matches_sort(native, sizes):
+    """gt_merge_runs: pairwise merge-path rounds over any number of sorted runs,
+    empty and ragged ones included, with heavy duplicates across runs."""
+    rng = np.random.default_rng(sum(sizes) + len(sizes))
+    runs = [np.sort(rng.integers(0, 1 << 16, size=m).astype(np.uint64) << np.uint64(40)
+                    | rng.integers(0, 4, size=m).astype(np.uint64)) for m in sizes]
+    keys = torch.from_numpy(np.concatenate(runs).view(np.int64).copy())
+    got = native.merge_runs(keys.cuda(), sizes).cpu()
+    assert np.array_equal(got.numpy().view(np.uint64), np.sort(keys.numpy().view(np.uint64)))
+    assert torch.equal(got, CpuOps().merge_runs(keys, sizes))
+
+
+def test_merge_runs_in_csr_runs_and_unsigned_order(native):
+    """Merging in-CSR runs gives the (dst, src) sort; keys with the top bit set
+    order as unsigned (the keys are uint64 bit patterns in int64 tensors)."""
+    rng = np.random.default_rng(11)
+    keys, sizes = _runs_by_dst_then_src(rng, 4, 20, [50_000, 1, 80_000, 20_000])
+    got = native.merge_runs(keys.cuda(), sizes).cpu()
+    assert torch.equal(got, native.sort_keys(keys.cuda(), 0, 40).cpu())
+    hi = np.uint64(1) << np.uint64(63)
+    a = np.sort(rng.integers(0, 1 << 62, 5000).astype(np.uint64) | hi)
+    b = np.sort(rng.integers(0, 1 << 62, 7000).astype(np.uint64))
+    k = torch.from_numpy(np.concatenate([a, b]).view(np.int64).copy())
+    got = native.merge_runs(k.cuda(), [a.size, b.size]).cpu().numpy().view(np.uint64)
+    assert np.array_equal(got, np.sort(np.concatenate([a, b])))
+
+
+def test_merge_runs_rejects_bad_offsets(native):
+    k = torch.arange(10, dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError):
+        native.merge_runs(k, [4, 5])  # sizes do not add up to n
+    with pytest.raises(ValueError):
+        native.merge_runs(k, [12, -2])
+
+
 def test_id_map_pack_swap_csr_match_cpu(native):
     rng = np.random.default_rng(3)
     src = torch.from_numpy(rng.integers(-500, 9000, size=20000))
