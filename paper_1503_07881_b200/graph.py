@@ -469,6 +469,7 @@ class DeviceGraph(_GraphReadAPI):
         self._handle = new
         self._n, self._e = _native.graph_sizes(new)
         self._host = None
+        self._ids = None
         self._finalizer = weakref.finalize(self, _native.graph_free, new)
 
     add_node = _mutating("add_node")
