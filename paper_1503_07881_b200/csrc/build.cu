@@ -23,6 +23,7 @@
 // convert.py:59 instead: radix sort of the 2R ids + unique + binary search.
 #include "graph.cuh"
 #include "radix_sort.cuh"
+#include "scan.cuh"
 #include "segment.cuh"
 
 #include <algorithm>
@@ -345,7 +346,121 @@ __global__ void gl_row_kernel(const int64_t* __restrict__ ids, const int32_t* __
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += stride)
     out[i] = ids[adj[begin + i]];
 }
+// Kept (distinct) keys per SEG_TILE tile of the sorted out-keys (scanned into
+// segment_kernel<true>'s tile bases), and the in-sort digit counts of the
+// dropped copies (see in_hist_kernel). Tiles are independent: no look-back.
+__global__ void __launch_bounds__(256) dedupe_count_kernel(const uint64_t* __restrict__ keys,
+                                                           int64_t n, int kbits, SortPlan in_plan,
+                                                           unsigned long long* __restrict__ dup_hist,
+                                                           int64_t* __restrict__ tile_cnt) {
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
+  __shared__ uint32_t s_w[8];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < in_plan.passes * 256; i += 256) sh[i] = 0;
+  __syncthreads();
+  const int64_t wbase = int64_t(blockIdx.x) * SEG_TILE + int64_t(warp) * 32 * SEG_KPT;
+  const uint64_t lowmask = (1ull << kbits) - 1ull;
+  uint64_t k[SEG_KPT];
+#pragma unroll
+  for (int i = 0; i < SEG_KPT; ++i) {
+    const int64_t idx = wbase + i * 32 + lane;
+    k[i] = idx < n ? ld_stream_u64(keys + idx) : 0ull;
+  }
+  uint64_t first_prev = 0;
+  if (lane == 0 && wbase > 0 && wbase - 1 < n) first_prev = keys[wbase - 1];
+  const unsigned lt = lanemask_lt();
+  uint32_t kept = 0;
+#pragma unroll
+  for (int i = 0; i < SEG_KPT; ++i) {
+    const int64_t idx = wbase + i * 32 + lane;
+    uint64_t prev = __shfl_up_sync(0xffffffffu, k[i], 1);
+    const uint64_t last_prev = __shfl_sync(0xffffffffu, i > 0 ? k[i > 0 ? i - 1 : 0] : first_prev, 31);
+    if (lane == 0) prev = (i == 0) ? first_prev : last_prev;
+    const bool valid = idx < n;
+    const bool keep = valid && (idx == 0 || k[i] != prev);
+    kept += __popc(__ballot_sync(0xffffffffu, keep));
+    // Copies of one key are adjacent lanes: the last lane of each run of
+    // dropped lanes adds the run length (equal addresses would serialise).
+    const uint32_t dropped = __ballot_sync(0xffffffffu, valid && !keep);
+    if (dropped && ((dropped >> lane) & 1u) && (lane == 31 || !((dropped >> (lane + 1)) & 1u))) {
+      const uint32_t below = ~dropped & lt;
+      const uint32_t cnt = uint32_t(lane) - (below ? uint32_t(31 - __clz(below)) : ~0u);
+      const uint64_t ik = ((k[i] & lowmask) << kbits) | (k[i] >> kbits);
+#pragma unroll
+      for (int q = 0; q < gt::RS_MAX_PASSES; ++q)
+        if (q < in_plan.passes)
+          atomicAdd(&sh[q * 256 + (uint32_t(ik >> in_plan.shift[q]) & ((1u << in_plan.bits[q]) - 1u))],
+                    cnt);
+    }
+  }
+  if (lane == 0) s_w[warp] = kept;
+  __syncthreads();
+  if (tid == 0) {
+    int64_t t = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += s_w[w];
+    tile_cnt[blockIdx.x] = t;
+  }
+  plan_hist_flush(sh, in_plan, dup_hist);
+}
+
+// The in-sort digit histograms without a per-key pass: the in-plan's digits
+// are the out-plan's digits restricted to the dst bits [0, kbits) (an in-key
+// is dst << kbits | src), so each in-histogram is a fold of one out-sort
+// histogram — counted by pack_kernel over every row — minus the digit counts
+// of the duplicates segment_kernel<true> dropped. grid = in passes.
+__global__ void __launch_bounds__(256) in_hist_kernel(const unsigned long long* __restrict__ out_hist,
+                                                      SortPlan in_plan, SortPlan src_pass,
+                                                      const unsigned long long* __restrict__ dup_hist,
+                                                      unsigned long long* __restrict__ in_hist) {
+  const int q = blockIdx.x;
+  const int b = in_plan.bits[q];
+  const int p = src_pass.shift[q];  // the out pass holding in-digit q (low bits of its digit)
+  const int w = src_pass.bits[q];   // that out digit's width
+  const uint32_t x = threadIdx.x;
+  if (x >= (1u << b)) {
+    if (x < 256) in_hist[q * 256 + x] = 0;
+    return;
+  }
+  unsigned long long c = 0;
+  for (uint32_t hi = 0; hi < (1u << (w - b)); ++hi) c += out_hist[p * 256 + (hi << b | x)];
+  in_hist[q * 256 + x] = c - dup_hist[q * 256 + x];
+}
+
 }  // namespace gtd
+
+namespace gt {
+
+// Out-sort digits (LSD first) for keys src << kb | dst: the dst bits in
+// near-equal digits, the last of them widened to 8 bits into the src bits,
+// then the rest of the src bits. The in-sort digits are the out digits cut to
+// the dst bits (in_hist_kernel), so this keeps them near-equal too (C4: out
+// 7,7,6,8,8,8,8 -> in 7,7,6,6) without adding a pass over make_plan.
+static SortPlan make_out_plan(int kb) {
+  SortPlan full = make_plan(0, 2 * kb);
+  if (kb <= 0) return full;
+  SortPlan p;
+  const int nd = (kb + 7) / 8;
+  int shift = 0;
+  for (int q = 0; q < nd; ++q) {
+    int b = kb / nd + (q < kb % nd ? 1 : 0);
+    if (q == nd - 1) b = std::min(8, 2 * kb - shift);
+    p.shift[p.passes] = shift;
+    p.bits[p.passes++] = b;
+    shift += b;
+  }
+  const int rest = 2 * kb - shift;
+  const int nr = (rest + 7) / 8;
+  for (int q = 0; q < nr; ++q) {
+    const int b = rest / nr + (q < rest % nr ? 1 : 0);
+    p.shift[p.passes] = shift;
+    p.bits[p.passes++] = b;
+    shift += b;
+  }
+  return p.passes <= full.passes ? p : full;
+}
+
+}  // namespace gt
 
 namespace gt {
 
@@ -525,7 +640,7 @@ gt_graph* build_csr(const int64_t* src, const int64_t* dst, int64_t rows, const 
     }
 
     // ---- out pass: pack -> sort (src,dst) -> dedupe/out-CSR/in-keys --------
-    SortPlan out_plan = make_plan(0, 2 * kb_bits);
+    SortPlan out_plan = make_out_plan(kb_bits);
     SortHist ho = sort_hist_begin(0);
     {
       Phase ph("build.pack", 24.0 * rows);
@@ -542,16 +657,30 @@ gt_graph* build_csr(const int64_t* src, const int64_t* dst, int64_t rows, const 
 
     g->out_adj = dalloc_n<int32_t>(rows);  // E <= rows; exact E known after dedupe
     g->out_off = dalloc_n<int64_t>(n_nodes + 1);
-    SortPlan in_plan = make_plan(kb_bits, 2 * kb_bits);
+    // in-plan digits = out-plan digits restricted to the dst bits (see in_hist_kernel)
+    SortPlan in_plan, src_pass;
+    for (int p = 0; p < out_plan.passes && out_plan.shift[p] < kb_bits; ++p) {
+      const int q = in_plan.passes++;
+      in_plan.shift[q] = kb_bits + out_plan.shift[p];
+      in_plan.bits[q] = std::min(out_plan.shift[p] + out_plan.bits[p], kb_bits) - out_plan.shift[p];
+      src_pass.shift[q] = p;
+      src_pass.bits[q] = out_plan.bits[p];
+    }
     SortHist hi_ = sort_hist_begin(1);
     {
-      Phase ph("build.dedupe", 8.0 * rows);
+      Phase ph("build.dedupe", 16.0 * rows);
       const int64_t tiles = ceil_div64(rows, gtd::SEG_TILE);
-      uint64_t* status = ws_n<uint64_t>(WS_LOOKBACK, size_t(tiles) * 256);
-      GT_CUDA(cudaMemsetAsync(counters + 18, 0, 4, s));
+      int64_t* tile_base = ws_n<int64_t>(WS_TMP3, size_t(tiles) + 1);
+      unsigned long long* dup = ws_n<unsigned long long>(WS_TMP4, RS_MAX_PASSES * 256);
+      GT_CUDA(cudaMemsetAsync(dup, 0, RS_MAX_PASSES * 256 * 8, s));
+      GT_LAUNCH(gtd::dedupe_count_kernel, static_cast<int>(tiles), 256, 0, sorted, rows, kb_bits,
+                in_plan, dup, tile_base);
+      exclusive_scan_i64(tile_base, tiles, small + 3);
       GT_LAUNCH(gtd::segment_kernel<true>, static_cast<int>(tiles), 256, 0, sorted, rows, kb_bits,
-                n_nodes, g->out_adj, g->out_off, other, in_plan, hi_.hist, status, counters + 18,
-                next_epoch(), small + 3);
+                n_nodes, g->out_adj, g->out_off, other, tile_base);
+      if (in_plan.passes)
+        GT_LAUNCH(gtd::in_hist_kernel, in_plan.passes, 256, 0, ho.hist, in_plan, src_pass, dup,
+                  hi_.hist);
     }
     const int64_t n_edges = read_i64(small + 3);
     g->e = n_edges;
@@ -565,9 +694,7 @@ gt_graph* build_csr(const int64_t* src, const int64_t* dst, int64_t rows, const 
       Phase ph("build.in_segment", 12.0 * n_edges + 8.0 * n_nodes);
       const int64_t tiles = ceil_div64(n_edges, gtd::SEG_TILE);
       GT_LAUNCH(gtd::segment_kernel<false>, static_cast<int>(tiles), 256, 0, in_sorted, n_edges,
-                kb_bits, n_nodes, g->in_adj, g->in_off, (uint64_t*)nullptr, SortPlan(),
-                (unsigned long long*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr, 0u,
-                (int64_t*)nullptr);
+                kb_bits, n_nodes, g->in_adj, g->in_off, (uint64_t*)nullptr, (const int64_t*)nullptr);
     }
     sync();
     return g;
@@ -955,8 +1082,7 @@ int gt_csr_from_keys(const uint64_t* d_sorted, int64_t m, int kbits, int64_t row
       keys = d_tmp;
     }
     GT_LAUNCH(gtd::segment_kernel<false>, ceil_div(m, gtd::SEG_TILE), 256, 0, keys, m, kbits,
-              rows, d_adj, d_off, (uint64_t*)nullptr, SortPlan(), (unsigned long long*)nullptr,
-              (uint64_t*)nullptr, (uint32_t*)nullptr, 0u, (int64_t*)nullptr);
+              rows, d_adj, d_off, (uint64_t*)nullptr, (const int64_t*)nullptr);
   }
   sync();
   GT_API_END

@@ -13,8 +13,11 @@ using gt::RS_TILE;
 
 // resident CTAs per SM the onesweep register budget is sized for
 constexpr int RS_MIN_BLOCKS = 3;
-// predecessor status words polled per look-back round trip
-constexpr int LB_WIN = 4;
+// predecessor status words polled per look-back round trip (GT_LB_WIN: sweeps)
+#ifndef GT_LB_WIN
+#define GT_LB_WIN 4
+#endif
+constexpr int LB_WIN = GT_LB_WIN;
 
 __global__ void __launch_bounds__(256) hist_kernel(const uint64_t* __restrict__ keys, int64_t n,
                                                    gt::SortPlan plan,
@@ -221,6 +224,229 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MIN_BLOCKS)
     onesweep_tile<BITS, RS_MATCH, false>(s, in, out, n, shift, digit_base, status, tile, epoch);
 }
 
+// ---- onesweep pass that ranks from shared memory -----------------------------
+// The kernel above loads its tile into registers and then ranks it; the keys
+// (32 registers) are what caps it at 80 registers = 3 CTAs per SM (ncu at C4:
+// 37% warps active, 2.6 TB/s, a fifth of the stall samples at the barrier
+// after the look-back). This one brings its tile into shared memory with ONE
+// bulk asynchronous copy (cp.async.bulk, completion counted on an mbarrier)
+// issued by one thread, and ranks it straight from there: no register
+// staging, no parking store, 64 registers. NT = 256 (4096-key tiles, 4 CTAs
+// per SM) or 512 (8192-key tiles, 2 CTAs per SM: half the look-backs).
+// Measured alternatives, not kept (profiles/r2s2_sort_kernel_variants.txt):
+// persistent CTAs double-buffering the next tile (the drawn tile waits a tile
+// time before publishing its aggregate, so successors' look-backs walk
+// further: slower in every placement of the draw), and a dedicated look-back
+// warp overlapping the in-tile scatter (one lane per 8 digits polls one
+// predecessor per round trip: 1.5x slower).
+#ifndef GT_SMEM_LB_WIN
+#define GT_SMEM_LB_WIN 2
+#endif
+constexpr int SMEM_LB_WIN = GT_SMEM_LB_WIN;
+
+template <int NT>
+struct OnesweepSmemT {
+  uint64_t keys[NT * RS_KPT];  // the tile by index, then scattered in place by position
+  uint32_t whist[NT / 32][256];
+  int64_t gbase[256];
+  unsigned long long bar;
+  uint32_t scan[NT / 32];
+  int tile;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+// Arm `bar` for `bytes` and start the bulk global->shared copy that completes it.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Exclusive scan across an NT-thread block; `sm` needs NT/32 slots.
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan_nt(uint32_t v, uint32_t* sm) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const uint32_t inc = warp_incl_scan(v);
+  if (l == 31) sm[w] = inc;
+  __syncthreads();
+  uint32_t wpre = 0;
+#pragma unroll
+  for (int i = 0; i < NT / 32; ++i)
+    if (i < w) wpre += sm[i];
+  __syncthreads();
+  return wpre + inc - v;
+}
+
+template <int BITS, int RS_MATCH, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT)
+    onesweep_smem_kernel(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int64_t n,
+                         int shift, const int64_t* __restrict__ digit_base,
+                         uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter,
+                         uint32_t epoch) {
+  constexpr int NW = NT / 32;
+  constexpr int TILE = NT * RS_KPT;
+  constexpr uint32_t mask = (1u << BITS) - 1u;
+  extern __shared__ __align__(128) unsigned char os1_dsm[];
+  OnesweepSmemT<NT>& s = *reinterpret_cast<OnesweepSmemT<NT>*>(os1_dsm);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    const int t = int(atomicAdd(tile_counter, 1u));
+    s.tile = t;
+    if (int64_t(t + 1) * TILE <= n) {
+      mbar_init(&s.bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      bulk_load(s.keys, in + int64_t(t) * TILE, TILE * 8, &s.bar);
+    }
+  }
+  for (int i = tid; i < NW * 256; i += NT) (&s.whist[0][0])[i] = 0;
+  __syncthreads();
+  const int cur = s.tile;
+  const int64_t base = int64_t(cur) * TILE;
+  const bool full = base + TILE <= n;
+  const int nvalid = full ? TILE : int(n - base);
+  const int woff = warp * 32 * RS_KPT + lane;  // key i of this thread: tile element woff + 32*i
+  int rem = nvalid - woff;
+  rem = rem > 32 * RS_KPT ? 32 * RS_KPT : (rem < 0 ? 0 : rem);
+  if (full) {
+    mbar_wait(&s.bar, 0);
+  } else {  // the last, partial tile: plain loads
+    for (int j = tid; j < nvalid; j += NT) s.keys[j] = ld_stream_u64(in + base + j);
+    __syncthreads();
+  }
+
+  // Stable ranks: peer masks (MATCH for RS_MATCH keys, one ballot per digit
+  // bit for the rest), then key by key the highest peer adds the group size to
+  // the warp's counter with one shared atomic and broadcasts the old value.
+  uint32_t rank[RS_KPT];
+  {
+    const unsigned lt = lanemask_lt();
+    uint32_t d[RS_KPT];
+#pragma unroll
+    for (int i = 0; i < RS_KPT; ++i) d[i] = uint32_t(s.keys[woff + 32 * i] >> shift) & mask;
+#pragma unroll
+    for (int i = 0; i < RS_KPT; ++i) {
+      if (i < RS_MATCH) {
+        rank[i] = full ? __match_any_sync(0xffffffffu, d[i])
+                       : __match_any_sync(0xffffffffu, 32 * i < rem ? d[i] : 0xFFFFu) &
+                             __ballot_sync(0xffffffffu, 32 * i < rem);
+      } else {
+        uint32_t peers = full ? 0xffffffffu : __ballot_sync(0xffffffffu, 32 * i < rem);
+#pragma unroll
+        for (int q = 0; q < BITS; ++q) {
+          const uint32_t bal = __ballot_sync(0xffffffffu, (d[i] >> q) & 1u);
+          peers &= ((d[i] >> q) & 1u) ? bal : ~bal;
+        }
+        rank[i] = peers;
+      }
+    }
+    uint32_t* wh = s.whist[warp];
+#pragma unroll
+    for (int i = 0; i < RS_KPT; ++i) {
+      const uint32_t peers = rank[i];
+      const int leader = 31 - __clz(peers);
+      uint32_t before = 0;
+      if (32 * i < rem && lane == leader) before = atomicAdd(&wh[d[i]], __popc(peers));
+      before = __shfl_sync(0xffffffffu, before, leader);
+      rank[i] = before + __popc(peers & lt);
+    }
+  }
+  __syncthreads();
+
+  uint32_t tile_cnt = 0;
+  if (tid < (1 << BITS)) {  // per digit: warp offsets, tile count, decoupled look-back
+    const int d = tid;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const uint32_t c = s.whist[w][d];
+      s.whist[w][d] = tile_cnt;
+      tile_cnt += c;
+    }
+    uint64_t* st = status + int64_t(cur) * 256 + d;
+    st_status_u64(st, lb_pack(cur == 0 ? LB_INC : LB_AGG, epoch, tile_cnt));
+    uint64_t excl = 0;
+    if (cur > 0) {
+      const uint64_t ep = uint64_t(epoch & 0x3FFFFFu);
+      int t = cur - 1;
+      bool done = false;
+      while (!done) {
+        uint64_t v[SMEM_LB_WIN];
+#pragma unroll
+        for (int q = 0; q < SMEM_LB_WIN; ++q)
+          v[q] = t - q >= 0 ? ld_status_u64(status + int64_t(t - q) * 256 + d) : 0ull;
+#pragma unroll
+        for (int q = 0; q < SMEM_LB_WIN; ++q) {
+          if (done || t < 0) break;
+          if (((v[q] >> 40) & 0x3FFFFFu) != ep || (v[q] >> 62) == 0) break;  // re-poll
+          excl += v[q] & ((1ull << 40) - 1);
+          if ((v[q] >> 62) == 2) done = true;
+          else --t;
+        }
+      }
+      st_status_u64(st, lb_pack(LB_INC, epoch, excl + tile_cnt));
+    }
+    s.gbase[d] = digit_base[d] + int64_t(excl);
+  }
+#ifdef GT_SMEM_LB_SYNC
+  __syncthreads();
+#endif
+  {  // in-tile digit starts (exclusive scan of the tile counts over the digits)
+    const uint32_t start = block_excl_scan_nt<NT>(tile_cnt, s.scan);
+    if (tid < (1 << BITS)) {
+      s.gbase[tid] -= int64_t(start);
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s.whist[w][tid] += start;
+    }
+  }
+  __syncthreads();
+  {
+    uint64_t k[RS_KPT];
+    uint32_t pos[RS_KPT];
+#pragma unroll
+    for (int i = 0; i < RS_KPT; ++i) {
+      k[i] = s.keys[woff + 32 * i];
+      pos[i] = s.whist[warp][uint32_t(k[i] >> shift) & mask] + rank[i];
+    }
+    __syncthreads();  // every key read before the buffer is reused by position
+#pragma unroll
+    for (int i = 0; i < RS_KPT; ++i)
+      if (32 * i < rem) s.keys[pos[i]] = k[i];
+  }
+  __syncthreads();
+  if (full) {
+#pragma unroll
+    for (int i = 0; i < RS_KPT; ++i) {
+      const int j = tid + i * NT;
+      const uint64_t key = s.keys[j];
+      out[s.gbase[uint32_t(key >> shift) & mask] + j] = key;
+    }
+  } else {
+    for (int j = tid; j < nvalid; j += NT) {
+      const uint64_t key = s.keys[j];
+      out[s.gbase[uint32_t(key >> shift) & mask] + j] = key;
+    }
+  }
+}
+
 }  // namespace gtd
 
 namespace gt {
@@ -273,6 +499,44 @@ static void launch_bits(int grid, const uint64_t* src, uint64_t* dst, int64_t n,
             n, shift, digit_base, status, counter, epoch);
 }
 
+// onesweep_smem_kernel with NT threads per CTA (tiles of NT * RS_KPT keys)
+template <int BITS, int M, int NT>
+static void launch_smem_bits(const uint64_t* src, uint64_t* dst, int64_t n, int shift,
+                             const int64_t* digit_base, uint64_t* status, uint32_t* counter,
+                             uint32_t epoch) {
+  constexpr auto kern = gtd::onesweep_smem_kernel<BITS, M, NT>;
+  constexpr size_t smem = sizeof(gtd::OnesweepSmemT<NT>);
+  static const bool once = [] {  // thread-safe one-time set-up
+    GT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    GT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    if (getenv("GT_SORT_DEBUG")) {
+      int b = 0;
+      GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, NT, smem));
+      fprintf(stderr, "onesweep_smem<%d,%d,%d>: %d CTAs/SM, %zu B smem\n", BITS, M, NT, b, smem);
+    }
+    return true;
+  }();
+  (void)once;
+  GT_LAUNCH(kern, static_cast<int>(ceil_div64(n, int64_t(NT) * RS_KPT)), NT, smem, src, dst, n,
+            shift, digit_base, status, counter, epoch);
+}
+
+template <int NT>
+static void launch_smem(int bits, const uint64_t* src, uint64_t* dst, int64_t n, int shift,
+                        const int64_t* digit_base, uint64_t* status, uint32_t* counter,
+                        uint32_t epoch) {
+  switch (bits) {
+#define GT_SMEM_CASE(B)                                                                      \
+  case B:                                                                                    \
+    launch_smem_bits<B, 6, NT>(src, dst, n, shift, digit_base, status, counter, epoch);      \
+    break;
+    GT_SMEM_CASE(1) GT_SMEM_CASE(2) GT_SMEM_CASE(3) GT_SMEM_CASE(4)
+    GT_SMEM_CASE(5) GT_SMEM_CASE(6) GT_SMEM_CASE(7) GT_SMEM_CASE(8)
+#undef GT_SMEM_CASE
+    default: fail(GT_EINVAL, "radix digit width must be 1..8");
+  }
+}
+
 template <int M>
 static void launch_m(int bits, int grid, const uint64_t* src, uint64_t* dst, int64_t n, int shift,
                      const int64_t* digit_base, uint64_t* status, uint32_t* counter,
@@ -293,6 +557,18 @@ static void launch_m(int bits, int grid, const uint64_t* src, uint64_t* dst, int
 static void launch_onesweep(int bits, int nmatch, int grid, const uint64_t* src, uint64_t* dst,
                             int64_t n, int shift, const int64_t* digit_base, uint64_t* status,
                             uint32_t* counter, uint32_t epoch) {
+  // GT_SORT_KERNEL (A/B measurements): 0 = the register-staged kernel,
+  // 1 = the shared-memory-ranked kernel with 256-thread CTAs, 2 = with
+  // 512-thread CTAs. The bulk copy needs 16-byte aligned tiles.
+  static const int kind = [] {
+    const char* env = getenv("GT_SORT_KERNEL");
+    return env ? atoi(env) : 1;
+  }();
+  if (kind > 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+    if (kind == 2) launch_smem<512>(bits, src, dst, n, shift, digit_base, status, counter, epoch);
+    else launch_smem<256>(bits, src, dst, n, shift, digit_base, status, counter, epoch);
+    return;
+  }
   if (nmatch <= 0)
     launch_m<0>(bits, grid, src, dst, n, shift, digit_base, status, counter, epoch);
   else if (nmatch >= RS_KPT)

@@ -30,25 +30,18 @@ __device__ __forceinline__ void warp_fill_gaps(bool have, int64_t first, int64_t
   }
 }
 
-// Sorted packed keys -> CSR rows. DEDUPE: drop repeated keys (convert.py:76-80),
-// emit in-keys (dst<<k|src) plus their digit histograms for the in-sort.
+// Sorted packed keys -> CSR rows. DEDUPE: drop repeated keys (convert.py:76-80)
+// and emit in-keys (dst<<k|src); the kept keys before each tile come from
+// dedupe_count_kernel + a scan (tile_base[t], tile_base[tiles] = total), so no
+// tile waits on its predecessors.
 template <bool DEDUPE>
 __global__ void __launch_bounds__(256, SEG_MIN_CTAS) segment_kernel(
     const uint64_t* __restrict__ keys, int64_t n, int kbits, int64_t n_rows,
     int32_t* __restrict__ adj, int64_t* __restrict__ off, uint64_t* __restrict__ in_keys,
-    SortPlan in_plan, unsigned long long* __restrict__ in_hist, uint64_t* __restrict__ status,
-    uint32_t* __restrict__ counter, uint32_t epoch, int64_t* __restrict__ total_out) {
-  __shared__ uint32_t sh[DEDUPE ? gt::RS_MAX_PASSES * 256 : 1];
+    const int64_t* __restrict__ tile_base) {
   __shared__ uint32_t s_warp[8];
-  __shared__ uint32_t s_tile;
-  __shared__ uint64_t s_excl;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (DEDUPE) {
-    for (int i = tid; i < in_plan.passes * 256; i += 256) sh[i] = 0;
-    if (tid == 0) s_tile = atomicAdd(counter, 1u);
-    __syncthreads();
-  }
-  const int tile = DEDUPE ? int(s_tile) : int(blockIdx.x);
+  const int tile = int(blockIdx.x);
   const int64_t wbase = int64_t(tile) * SEG_TILE + int64_t(warp) * 32 * SEG_KPT;
   const uint64_t lowmask = (1ull << kbits) - 1ull;
 
@@ -87,20 +80,12 @@ __global__ void __launch_bounds__(256, SEG_MIN_CTAS) segment_kernel(
   if (DEDUPE) {
     if (lane == 0) s_warp[warp] = run;
     __syncthreads();
-    uint32_t wpre = 0, tcount = 0;
+    uint32_t wpre = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      const uint32_t c = s_warp[w];
-      if (w < warp) wpre += c;
-      tcount += c;
-    }
-    if (tid == 0) s_excl = lookback_single(status, tile, epoch, tcount);
-    __syncthreads();
-    base_pos = int64_t(s_excl) + wpre;
-    if (int64_t(tile) == (n - 1) / SEG_TILE) {
-      total = int64_t(s_excl) + tcount;
-      if (tid == 0) *total_out = total;
-    }
+    for (int w = 0; w < 8; ++w)
+      if (w < warp) wpre += s_warp[w];
+    base_pos = tile_base[tile] + wpre;
+    total = tile_base[gridDim.x];
   } else {
     base_pos = wbase;
   }
@@ -115,11 +100,7 @@ __global__ void __launch_bounds__(256, SEG_MIN_CTAS) segment_kernel(
     const uint64_t col = k[i] & lowmask;
     if (keep) {
       adj[pos] = int32_t(col);
-      if (DEDUPE) {
-        const uint64_t ik = (col << kbits) | uint64_t(row);
-        in_keys[pos] = ik;
-        plan_hist_add(sh, in_plan, ik);
-      }
+      if (DEDUPE) in_keys[pos] = (col << kbits) | uint64_t(row);
     }
     // Row starts: rows (prev_row, row] begin at pos (empty rows share it).
     uint64_t prev = __shfl_up_sync(0xffffffffu, k[i], 1);
@@ -132,10 +113,6 @@ __global__ void __launch_bounds__(256, SEG_MIN_CTAS) segment_kernel(
     // Trailing rows (last_row, n_rows] end at the edge count.
     const bool tail = idx == n - 1;
     warp_fill_gaps(tail, row + 1, n_rows, total, off);
-  }
-  if (DEDUPE) {
-    __syncthreads();
-    plan_hist_flush(sh, in_plan, in_hist);
   }
 }
 

@@ -68,6 +68,20 @@ def test_duplicates_collapse_and_empty():
     assert e.node_count == 0 and e.edge_count == 0 and e.node_ids() == []
 
 
+@pytest.mark.parametrize("distinct,rows", [(1, 300_000), (7, 500_000), (5000, 2_000_000),
+                                           (200_000, 3_000_000)])
+def test_duplicate_heavy_tables_vs_oracle(distinct, rows):
+    """The in-sort histograms are the out-sort's minus the dropped duplicates'
+    digit counts: tables made mostly of copies (runs of one key spanning
+    warps and tiles, a single key repeated 300K times) must still sort exactly."""
+    rng = np.random.default_rng(distinct)
+    pairs = rng.integers(0, max(2, int(np.sqrt(distinct) * 40)), size=(distinct, 2))
+    pick = rng.integers(0, distinct, size=rows)
+    src, dst = pairs[pick, 0].astype(np.int64), pairs[pick, 1].astype(np.int64)
+    g = build(src, dst, device=True)
+    assert_csr_equal(g.csr(), ref.build_csr(src, dst), f"dups-{distinct}")
+
+
 def test_self_loops_and_negatives():
     g = build([-5, -5], [-5, 3])
     assert g.has_edge(-5, -5) and g.has_edge(-5, 3) and not g.has_edge(3, -5)
