@@ -49,7 +49,10 @@ constexpr int TC_ROWS_CAP = TC_CAND_TILE + 2;  // staged row offsets per tile
 constexpr int TC_SLOTS = 2048;                 // hash slots per warp (8 KB)
 constexpr int TC_WARP_MAX = TC_SLOTS / 4;      // largest d+(v) of a warp hash task
 constexpr int TC_CHUNK = 256;                  // arcs per warp task
-constexpr int TC_CHUNK_CTA = 16384;           // arcs per CTA task (swept at C4: 1024 -> 16384 = 219 -> 183 ms)
+#ifndef GT_TC_CHUNK_CTA
+#define GT_TC_CHUNK_CTA 16384
+#endif
+constexpr int TC_CHUNK_CTA = GT_TC_CHUNK_CTA;  // arcs per CTA task (v order, C4: 1024 -> 16384 = 219 -> 183 ms)
 constexpr int TC_BM_BITS = TC_SLOTS * 32;      // per-warp bitmap window (same 8 KB region)
 constexpr int TC_SPLIT_TOP = TC_BM_BITS / 2;   // split tables: bitmap of the top 2^15 ranks ...
 constexpr int TC_SPLIT_SLOTS = TC_SLOTS / 2;   // ... + hash of the rest (4 KB each)
@@ -856,6 +859,33 @@ __global__ void __launch_bounds__(256) tc_stats_kernel(const int64_t* __restrict
   atomicAdd(&out[kind * 4 + 3], (unsigned long long)dm);
 }
 
+// Bitmap tasks reordered by the adj_p position of their first arc (the rank
+// of its u), so that the warps running at the same time walk N+(u) suffixes
+// of nearby u: the suffix data of the tasks in flight stays in L2. In v order
+// (tasks of one v adjacent, so a warp reuses its table) every task walks ~256
+// scattered N+(u) lists and ncu at C4 showed 656 GB of DRAM reads at a 26%
+// L2 hit rate in the count kernel; in u order the table is rebuilt per task
+// (clearing <= 8 KB and setting d+(v) bits), small against ~10^5 probes.
+__global__ void __launch_bounds__(256) tc_task_keys_kernel(const int2* __restrict__ tasks,
+                                                           int64_t nt, int chunk,
+                                                           const int64_t* __restrict__ off_m,
+                                                           const int2* __restrict__ nm,
+                                                           uint64_t* __restrict__ keys) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  const int2 t = tasks[i];
+  const int32_t a = nm[off_m[t.x] + int64_t(t.y) * chunk].x;
+  keys[i] = (uint64_t(uint32_t(a)) << 32) | uint64_t(i);
+}
+
+__global__ void __launch_bounds__(256) tc_task_permute_kernel(const uint64_t* __restrict__ keys,
+                                                              int64_t nt,
+                                                              const int2* __restrict__ tasks,
+                                                              int2* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < nt) out[i] = tasks[keys[i] & 0xffffffffull];
+}
+
 __global__ void __launch_bounds__(256) tc_task_fill_kernel(const int64_t* __restrict__ toff,
                                                            int64_t n, int2* __restrict__ tasks) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1585,6 +1615,27 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
     if (n_ct)
       GT_LAUNCH(gtd::tc_task_fill_kernel, ceil_div(n, 256), 256, 0, t2, n, tasks + n_bm + n_wt);
   }
+  static const bool order_by_u = [] {  // GT_TC_ORDER=0: bitmap tasks in v order (A/B)
+    const char* env = getenv("GT_TC_ORDER");
+    return !(env && atoi(env) == 0);
+  }();
+  auto order_tasks = [&](int2* tk, int64_t nt, int chunk) {
+    Phase ph("tc.tasks", 40.0 * nt);
+    uint64_t* ka = ws_n<uint64_t>(WS_KEYS_A, size_t(nt));
+    uint64_t* kb = ws_n<uint64_t>(WS_KEYS_B, size_t(nt));
+    GT_LAUNCH(gtd::tc_task_keys_kernel, ceil_div(nt, 256), 256, 0, tk, nt, chunk, off_m, nm, ka);
+    SortPlan plan = make_plan(32, 32 + bits_for(m + 1));
+    SortHist hs = sort_hist_begin(0);
+    sort_histogram(ka, nt, plan, hs);
+    uint64_t* srt = radix_sort(ka, kb, nt, plan, hs, "tc.tasks");
+    int2* tmp = reinterpret_cast<int2*>(srt == ka ? kb : ka);
+    GT_LAUNCH(gtd::tc_task_permute_kernel, ceil_div(nt, 256), 256, 0, srt, nt, tk, tmp);
+    GT_CUDA(cudaMemcpyAsync(tk, tmp, size_t(nt) * sizeof(int2), cudaMemcpyDeviceToDevice, s));
+  };
+  if (order_by_u && n_bm > 1) order_tasks(tasks, n_bm, gtd::TC_CHUNK);
+  // (the CTA tasks are left in v order: in u order, with chunks of 2048..16384
+  // arcs, they measured 198-207 ms against 193 at C4 — a chunk of a long
+  // N-(v) list spans most of the u range, so tasks in flight share little)
   unsigned long long* total = reinterpret_cast<unsigned long long*>(small + 6);
   GT_CUDA(cudaMemsetAsync(total, 0, 8, s));
   if (n_bm + n_wt) {

@@ -1,0 +1,11 @@
+#!/bin/bash
+# CTA triangle tasks in u order: chunk-size sweep at C4 (+ parity at the default)
+cd "$GRAFT_REPO_ROOT"
+mkdir -p gpurun_out
+T=${1:-s2tcc}
+timeout 900 python -m pytest -x -q tests/test_triangles_gpu.py -m gpu > gpurun_out/${T}_pytest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/${T}_pytest.log
+for V in "" cc2048 cc4096 cc8192; do
+  GT_LIB_VARIANT=$V timeout 300 python scripts/prof_tc.py c4 2 > gpurun_out/${T}_c4_${V:-cc16384}.log 2>&1
+done
+echo done
