@@ -1018,7 +1018,49 @@ constexpr int TC_WIN = 7;
 constexpr int TC_LONG = 64;
 constexpr int TC_UNROLL = 4;
 
-template <typename Probe, typename T = int32_t>
+// The part of a long suffix past its first 32*TC_UNROLL elements, walked by
+// the warp with 16-byte vector loads (4 ranks per load): at C4 most probes
+// land here (ncu: the scalar walk's load, bounds test and select cost as many
+// instructions as the probe itself). Unaligned head and short rest by single
+// loads. Used by the CTA count kernel only (see tc_wedges32).
+template <typename Probe, typename T>
+__device__ __forceinline__ uint32_t tc_long_tail(const T* __restrict__ p, int len,
+                                                 const Probe& probe) {
+  constexpr int VE = 16 / int(sizeof(T));
+  const int lane = threadIdx.x & 31;
+  uint32_t cnt = 0;
+  const int mis = int((reinterpret_cast<uintptr_t>(p) & 15u) / sizeof(T));
+  const int head = min(len, mis ? VE - mis : 0);
+  if (lane < head) cnt += probe(int32_t(__ldg(p + lane))) ? 1u : 0u;
+  p += head;
+  len -= head;
+  const int nv = len / VE;
+  const uint4* pv = reinterpret_cast<const uint4*>(p);
+  auto probe_vec = [&](const uint4 q) {
+    const uint32_t x[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      if (sizeof(T) == 2) {
+        cnt += probe(int32_t(x[h] & 0xffffu)) ? 1u : 0u;
+        cnt += probe(int32_t(x[h] >> 16)) ? 1u : 0u;
+      } else {
+        cnt += probe(int32_t(x[h])) ? 1u : 0u;
+      }
+    }
+  };
+  int j = lane;
+  for (; j + 32 < nv; j += 64) {  // two loads in flight per lane
+    const uint4 a = __ldg(pv + j), b = __ldg(pv + j + 32);
+    probe_vec(a);
+    probe_vec(b);
+  }
+  if (j < nv) probe_vec(__ldg(pv + j));
+  const int rest = len - nv * VE;
+  if (lane < rest) cnt += probe(int32_t(__ldg(p + nv * VE + lane))) ? 1u : 0u;
+  return cnt;
+}
+
+template <typename Probe, typename T = int32_t, bool VEC = false>
 __device__ __forceinline__ uint32_t tc_wedges32(const T* __restrict__ adj, int2 suffix,
                                                 const Probe& probe,
                                                 uint8_t* s_start /* [32 * TC_WIN] */) {
@@ -1052,16 +1094,21 @@ __device__ __forceinline__ uint32_t tc_wedges32(const T* __restrict__ adj, int2 
 #pragma unroll
       for (int q = 0; q < TC_UNROLL; ++q)
         if (wa[q] != TC_EMPTY) cnt += probe(wa[q]) ? 1u : 0u;
-      for (int k0 = 32 * TC_UNROLL; k0 < la; k0 += 32 * TC_UNROLL) {  // rare: long tails
-        int32_t w[TC_UNROLL];
+      if (VEC) {  // vector walk: C4 CTA count 193 -> 180 ms; slower in the warp kernel
+        // (16-bit window ranks: 357 vs 307 ms; split / hash tasks: +20 ms)
+        if (la > 32 * TC_UNROLL) cnt += tc_long_tail(ba + 32 * TC_UNROLL, la - 32 * TC_UNROLL, probe);
+      } else {
+        for (int k0 = 32 * TC_UNROLL; k0 < la; k0 += 32 * TC_UNROLL) {
+          int32_t w[TC_UNROLL];
 #pragma unroll
-        for (int q = 0; q < TC_UNROLL; ++q) {
-          const int k = k0 + 32 * q + lane;
-          w[q] = k < la ? int32_t(__ldg(ba + k)) : TC_EMPTY;
+          for (int q = 0; q < TC_UNROLL; ++q) {
+            const int k = k0 + 32 * q + lane;
+            w[q] = k < la ? int32_t(__ldg(ba + k)) : TC_EMPTY;
+          }
+#pragma unroll
+          for (int q = 0; q < TC_UNROLL; ++q)
+            if (w[q] != TC_EMPTY) cnt += probe(w[q]) ? 1u : 0u;
         }
-#pragma unroll
-        for (int q = 0; q < TC_UNROLL; ++q)
-          if (w[q] != TC_EMPTY) cnt += probe(w[q]) ? 1u : 0u;
       }
       i = j;
       ba = bb;
@@ -1263,7 +1310,7 @@ __global__ void __launch_bounds__(256) tc_count_cta_kernel(
       if (jb >= end) break;
       const int jj = jb + lane;
       const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
-      cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
+      cnt += tc_wedges32<decltype(probe), int32_t, true>(adj_p, sfx, probe, s_start[warp]);
     }
     acc += cnt;
   };
