@@ -355,6 +355,27 @@ GT_API int gt_pagerank_step(const int64_t* d_in_off, const int32_t* d_in_adj, in
  * the rank-space orientation: the parts of all ranks sum to gt_triangles
  * (the all-reduce is the caller's). */
 GT_API int gt_triangles_part(const gt_graph* g, int part, int nparts, int64_t* count);
+/* Sharded orientation (distributed.triangle_count): a rank holds the
+ * undirected rows of the ids [row_lo, row_lo + rows) (local offsets d_off,
+ * global neighbour ids d_adj).
+ * gt_tc_undirected_keys: both directions of every edge, self-loops dropped,
+ * as (u << kbits | v) keys (d_keys: capacity 2 * d_off[rows]); *n_keys is the
+ * count written (replaces Graph.undirected_neighbors, graphs.py:163-167, once
+ * sorted, deduped and shuffled by row).
+ * gt_tc_degree_rank: d_rank[id] = position of id in (degree, id) order of the
+ * n degrees (algorithms.py:103-106).
+ * gt_tc_orient_keys: the arcs to higher-ranked neighbours as
+ * (rank(u) << kbits | rank(v)) (algorithms.py:108; capacity d_off[rows]).
+ * gt_triangles_oriented_part: gt_triangles_part over a caller-built
+ * rank-space orientation (d_off_p int64[n+1], d_adj_p int32[m], rows sorted). */
+GT_API int gt_tc_undirected_keys(const int64_t* d_off, const int32_t* d_adj, int64_t rows,
+                                 int64_t row_lo, int kbits, uint64_t* d_keys, int64_t* n_keys);
+GT_API int gt_tc_degree_rank(const int64_t* d_deg, int64_t n, int32_t* d_rank);
+GT_API int gt_tc_orient_keys(const int64_t* d_off, const int32_t* d_adj, int64_t rows,
+                             int64_t row_lo, const int32_t* d_rank, int kbits, uint64_t* d_keys,
+                             int64_t* m_keys);
+GT_API int gt_triangles_oriented_part(const int64_t* d_off_p, const int32_t* d_adj_p, int64_t n,
+                                      int64_t m, int part, int nparts, int64_t* count);
 /* Undirected simple-edge count m of the graph (self-loops dropped, reciprocal
  * pairs merged: the size of the orientation the triangle count builds), or -1
  * when no triangle count has run on g yet (bench unit: undirected edges/s). */

@@ -98,6 +98,13 @@ SIGNATURES = {
                                         _VP, _VP, _VP, ctypes.c_double, ctypes.c_int, _VP, _VP,
                                         _VP]),
     "gt_triangles_part": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, _I64P]),
+    "gt_tc_undirected_keys": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_int64,
+                                             ctypes.c_int, _VP, _I64P]),
+    "gt_tc_degree_rank": (ctypes.c_int, [_VP, ctypes.c_int64, _VP]),
+    "gt_tc_orient_keys": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_int64, _VP,
+                                         ctypes.c_int, _VP, _I64P]),
+    "gt_triangles_oriented_part": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_int64,
+                                                  ctypes.c_int, ctypes.c_int, _I64P]),
     "gt_graph_undirected_edges": (ctypes.c_int, [_VP, _I64P]),
     "gt_select_rows": (ctypes.c_int, [_VP, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int64, ctypes.c_double, _VP, ctypes.c_int64, _VP,

@@ -1359,6 +1359,133 @@ __global__ void __launch_bounds__(256) tc_count_cta_kernel(
   if (threadIdx.x == 0 && acc) atomicAdd(total, acc);
 }
 
+// ---- sharded orientation (distributed.triangle_count) ------------------------
+// A rank holds the undirected rows of an id range [row_lo, row_lo + rows)
+// (local offsets, global neighbour ids). Warp per row; outputs compacted in
+// row order with ballots after a count pass and a scan.
+
+// 2 x (neighbours other than the row itself): both directions of every edge.
+__global__ void __launch_bounds__(256) tc_und_count_kernel(const int64_t* __restrict__ off,
+                                                           const int32_t* __restrict__ adj,
+                                                           int64_t rows, int64_t row_lo,
+                                                           int64_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = int64_t(gridDim.x) * 8;
+  for (int64_t r = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5); r < rows; r += nw) {
+    const int32_t u = int32_t(row_lo + r);
+    int c = 0;
+    for (int64_t j = off[r] + lane; j < off[r + 1]; j += 32) c += adj[j] != u;
+    c = warp_sum(c);
+    if (lane == 0) cnt[r] = 2 * int64_t(c);
+  }
+}
+
+__global__ void __launch_bounds__(256) tc_und_write_kernel(const int64_t* __restrict__ off,
+                                                           const int32_t* __restrict__ adj,
+                                                           int64_t rows, int64_t row_lo, int kbits,
+                                                           const int64_t* __restrict__ pos,
+                                                           uint64_t* __restrict__ keys) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  const int64_t nw = int64_t(gridDim.x) * 8;
+  for (int64_t r = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5); r < rows; r += nw) {
+    const uint64_t u = uint64_t(row_lo + r);
+    int64_t o = pos[r];
+    for (int64_t j0 = off[r]; j0 < off[r + 1]; j0 += 32) {
+      const int64_t j = j0 + lane;
+      const uint64_t x = j < off[r + 1] ? uint64_t(uint32_t(adj[j])) : u;
+      const bool keep = x != u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int64_t k = o + 2 * __popc(bal & lt);
+        keys[k] = (u << kbits) | x;
+        keys[k + 1] = (x << kbits) | u;
+      }
+      o += 2 * __popc(bal);
+    }
+  }
+}
+
+// Arcs to higher-ranked neighbours: (rank(u) << kbits | rank(v)).
+__global__ void __launch_bounds__(256) tc_orient_count_kernel(const int64_t* __restrict__ off,
+                                                              const int32_t* __restrict__ adj,
+                                                              int64_t rows, int64_t row_lo,
+                                                              const int32_t* __restrict__ rank,
+                                                              int64_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = int64_t(gridDim.x) * 8;
+  for (int64_t r = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5); r < rows; r += nw) {
+    const int32_t ru = rank[row_lo + r];
+    int c = 0;
+    for (int64_t j = off[r] + lane; j < off[r + 1]; j += 32) c += rank[adj[j]] > ru;
+    c = warp_sum(c);
+    if (lane == 0) cnt[r] = c;
+  }
+}
+
+__global__ void __launch_bounds__(256) tc_orient_write_kernel(const int64_t* __restrict__ off,
+                                                              const int32_t* __restrict__ adj,
+                                                              int64_t rows, int64_t row_lo,
+                                                              const int32_t* __restrict__ rank,
+                                                              int kbits,
+                                                              const int64_t* __restrict__ pos,
+                                                              uint64_t* __restrict__ keys) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  const int64_t nw = int64_t(gridDim.x) * 8;
+  for (int64_t r = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5); r < rows; r += nw) {
+    const int32_t ru = rank[row_lo + r];
+    int64_t o = pos[r];
+    for (int64_t j0 = off[r]; j0 < off[r + 1]; j0 += 32) {
+      const int64_t j = j0 + lane;
+      const int32_t rv = j < off[r + 1] ? rank[adj[j]] : -1;
+      const bool keep = rv > ru;
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) keys[o + __popc(bal & lt)] = (uint64_t(uint32_t(ru)) << kbits) | uint64_t(uint32_t(rv));
+      o += __popc(bal);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) deg64_to_32_kernel(const int64_t* __restrict__ d, int64_t n,
+                                                          int32_t* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = int32_t(d[i]);
+}
+
+// N-(v) sizes of the middle vertices this part owns (v = part mod nparts).
+__global__ void __launch_bounds__(256) tc_owned_indeg_kernel(const int32_t* __restrict__ adj_p,
+                                                             int64_t m, int part, int nparts,
+                                                             unsigned long long* __restrict__ dm) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t a = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; a < m; a += stride) {
+    const int32_t v = adj_p[a];
+    if (v % nparts == part) atomicAdd(&dm[v], 1ull);
+  }
+}
+
+// Warp per rank-row u: every arc (u, v) with an owned v filed under N-(v) as
+// (a+1, remaining length of N+(u)) — place_rows_kernel without the move.
+__global__ void __launch_bounds__(256) tc_file_owned_kernel(const int64_t* __restrict__ off_p,
+                                                            const int32_t* __restrict__ adj_p,
+                                                            int64_t n, int part, int nparts,
+                                                            const int64_t* __restrict__ off_m,
+                                                            unsigned int* __restrict__ cur,
+                                                            int2* __restrict__ nm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = int64_t(gridDim.x) * 8;
+  for (int64_t u = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5); u < n; u += nw) {
+    const int64_t a0 = off_p[u];
+    const int cnt = int(off_p[u + 1] - a0);
+    for (int t = lane; t < cnt; t += 32) {
+      const int32_t v = adj_p[a0 + t];
+      if (v % nparts != part) continue;
+      const unsigned slot = atomicAdd(&cur[v], 1u);
+      nm[off_m[v] + slot] = make_int2(int(a0 + t + 1), cnt - t - 1);
+    }
+  }
+}
+
 }  // namespace gtd
 
 namespace gt {
@@ -1582,6 +1709,8 @@ void triangle_orientation(const gt_graph* g, int32_t* h_deg, int32_t* h_rank, in
   sync();
 }
 
+static int64_t count_oriented(const Oriented& o, int part, int nparts);
+
 int64_t triangles(const gt_graph* g, int part, int nparts) {
   require_init();
   if (nparts < 1 || part < 0 || part >= nparts) fail(GT_EINVAL, "part must be in [0, nparts)");
@@ -1592,8 +1721,17 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
   int64_t* small = ws_n<int64_t>(WS_SMALL, 16);
   uint32_t* counters = ws_n<uint32_t>(WS_COUNTERS, 64);
   const Oriented o = orient(g);
-  const int64_t m = o.m;
-  g->m_und = m;
+  g->m_und = o.m;
+  return count_oriented(o, part, nparts);
+}
+
+// The count over an orientation (rank space: N+ rows, N- lists of the middle
+// vertices v = part mod nparts).
+static int64_t count_oriented(const Oriented& o, int part, int nparts) {
+  const int64_t n = o.n, m = o.m;
+  cudaStream_t s = ctx().stream;
+  int64_t* small = ws_n<int64_t>(WS_SMALL, 16);
+  uint32_t* counters = ws_n<uint32_t>(WS_COUNTERS, 64);
   if (m == 0) return 0;
   if (m >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangles: >= 2^31 undirected edges");
 
@@ -1739,6 +1877,102 @@ int64_t triangles(const gt_graph* g, int part, int nparts) {
   return result;
 }
 
+// Sharded orientation primitives (distributed.triangle_count); see the
+// kernels above and include/gtb200.h.
+int64_t tc_undirected_keys(const int64_t* off, const int32_t* adj, int64_t rows, int64_t row_lo,
+                           int kbits, uint64_t* keys) {
+  require_init();
+  if (rows <= 0) return 0;
+  int64_t* cnt = ws_n<int64_t>(WS_TMP3, size_t(rows) + 1);
+  int64_t* small = ws_n<int64_t>(WS_SMALL, 16);
+  const int grid = grid_cap(ceil_div64(rows, 8));
+  GT_LAUNCH(gtd::tc_und_count_kernel, grid, 256, 0, off, adj, rows, row_lo, cnt);
+  exclusive_scan_i64(cnt, rows, small + 2);
+  GT_LAUNCH(gtd::tc_und_write_kernel, grid, 256, 0, off, adj, rows, row_lo, kbits, cnt, keys);
+  int64_t total = 0;
+  d2h(&total, small + 2, 8);
+  sync();
+  return total;
+}
+
+int64_t tc_orient_keys(const int64_t* off, const int32_t* adj, int64_t rows, int64_t row_lo,
+                       const int32_t* rank, int kbits, uint64_t* keys) {
+  require_init();
+  if (rows <= 0) return 0;
+  int64_t* cnt = ws_n<int64_t>(WS_TMP3, size_t(rows) + 1);
+  int64_t* small = ws_n<int64_t>(WS_SMALL, 16);
+  const int grid = grid_cap(ceil_div64(rows, 8));
+  GT_LAUNCH(gtd::tc_orient_count_kernel, grid, 256, 0, off, adj, rows, row_lo, rank, cnt);
+  exclusive_scan_i64(cnt, rows, small + 2);
+  GT_LAUNCH(gtd::tc_orient_write_kernel, grid, 256, 0, off, adj, rows, row_lo, rank, kbits, cnt,
+            keys);
+  int64_t total = 0;
+  d2h(&total, small + 2, 8);
+  sync();
+  return total;
+}
+
+// rank[id] = position of id in (degree, id) order (algorithms.py:103-106).
+void tc_degree_rank(const int64_t* deg, int64_t n, int32_t* rank) {
+  require_init();
+  if (n <= 0) return;
+  if (n >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "degree rank: >= 2^31 nodes");
+  int32_t* d32 = ws_n<int32_t>(WS_TMP3, size_t(n) * 2);
+  int32_t* order = d32 + n;
+  int64_t* small = ws_n<int64_t>(WS_SMALL, 16);
+  GT_LAUNCH(gtd::deg64_to_32_kernel, ceil_div(n, 256), 256, 0, deg, n, d32);
+  GT_CUDA(cudaMemsetAsync(small + 12, 0, 8, ctx().stream));
+  GT_LAUNCH(gtd::max_i32_kernel, grid_cap(ceil_div64(n, 256)), 256, 0, d32, n,
+            reinterpret_cast<int*>(small + 12));
+  int64_t mx = 0;
+  d2h(&mx, small + 12, 8);
+  sync();
+  const int kbits = bits_for(n);
+  uint64_t* ka = ws_n<uint64_t>(WS_KEYS_A, size_t(n));
+  uint64_t* kb = ws_n<uint64_t>(WS_KEYS_B, size_t(n));
+  SortPlan plan = make_plan(0, kbits + bits_for(int64_t(mx & 0xffffffff) + 1));
+  SortHist h = sort_hist_begin(0);
+  GT_LAUNCH(gtd::rank_keys_kernel, grid_cap(ceil_div64(n, 1024)), 256, 0, d32, n, kbits, plan,
+            h.hist, ka);
+  uint64_t* sorted = radix_sort(ka, kb, n, plan, h, "tc.sort");
+  GT_LAUNCH(gtd::rank_scatter_kernel, ceil_div(n, 256), 256, 0, sorted, n,
+            (uint64_t(1) << kbits) - 1, rank, order);
+  sync();
+}
+
+// Triangles whose middle vertex v = part (mod nparts), from a rank-space
+// orientation given by the caller (replicated N+ rows).
+int64_t triangles_oriented(const int64_t* off_p, const int32_t* adj_p, int64_t n, int64_t m,
+                           int part, int nparts) {
+  require_init();
+  if (nparts < 1 || part < 0 || part >= nparts) fail(GT_EINVAL, "part must be in [0, nparts)");
+  if (n <= 0 || m <= 0) return 0;
+  if (n >= (int64_t(1) << 31)) fail(GT_ECAPACITY, "triangles: >= 2^31 nodes");
+  cudaStream_t s = ctx().stream;
+  Oriented o;
+  o.n = n;
+  o.m = m;
+  o.kbits = bits_for(n);
+  o.off_p = const_cast<int64_t*>(off_p);
+  o.adj_p = const_cast<int32_t*>(adj_p);
+  char* p = static_cast<char*>(ws_get(WS_TMP3, size_t(n + 1) * 8 + size_t(n) * 4 + 64));
+  o.off_m = reinterpret_cast<int64_t*>(p);
+  unsigned int* cur = reinterpret_cast<unsigned int*>(p + ((size_t(n + 1) * 8 + 15) & ~size_t(15)));
+  int64_t* small = ws_n<int64_t>(WS_SMALL, 16);
+  GT_CUDA(cudaMemsetAsync(o.off_m, 0, size_t(n + 1) * 8, s));
+  GT_LAUNCH(gtd::tc_owned_indeg_kernel, grid_cap(ceil_div64(m, 256)), 256, 0, adj_p, m, part,
+            nparts, reinterpret_cast<unsigned long long*>(o.off_m));
+  exclusive_scan_i64(o.off_m, n, small + 3);
+  int64_t owned = 0;
+  d2h(&owned, small + 3, 8);
+  sync();
+  o.nm = reinterpret_cast<int2*>(ws_get(WS_TMP1, size_t(std::max<int64_t>(owned, 1)) * 8 + 16));
+  GT_CUDA(cudaMemsetAsync(cur, 0, size_t(n) * 4, s));
+  GT_LAUNCH(gtd::tc_file_owned_kernel, grid_cap(ceil_div64(n, 8)), 256, 0, off_p, adj_p, n, part,
+            nparts, o.off_m, cur, o.nm);
+  return count_oriented(o, part, nparts);
+}
+
 }  // namespace gt
 
 using namespace gt;
@@ -1763,6 +1997,41 @@ int gt_triangles_part(const gt_graph* g, int part, int nparts, int64_t* count) {
   GT_API_BEGIN
   if (!count) fail(GT_EINVAL, "count must not be NULL");
   *count = triangles(g, part, nparts);
+  GT_API_END
+}
+
+int gt_tc_undirected_keys(const int64_t* d_off, const int32_t* d_adj, int64_t rows, int64_t row_lo,
+                          int kbits, uint64_t* d_keys, int64_t* n_keys) {
+  GT_API_BEGIN
+  if (!n_keys || (rows > 0 && (!d_off || !d_adj || !d_keys))) fail(GT_EINVAL, "null argument");
+  if (kbits < 1 || kbits > 31) fail(GT_EINVAL, "kbits must be in [1, 31]");
+  *n_keys = tc_undirected_keys(d_off, d_adj, rows, row_lo, kbits, d_keys);
+  GT_API_END
+}
+
+int gt_tc_degree_rank(const int64_t* d_deg, int64_t n, int32_t* d_rank) {
+  GT_API_BEGIN
+  if (n > 0 && (!d_deg || !d_rank)) fail(GT_EINVAL, "null argument");
+  tc_degree_rank(d_deg, n, d_rank);
+  GT_API_END
+}
+
+int gt_tc_orient_keys(const int64_t* d_off, const int32_t* d_adj, int64_t rows, int64_t row_lo,
+                      const int32_t* d_rank, int kbits, uint64_t* d_keys, int64_t* m_keys) {
+  GT_API_BEGIN
+  if (!m_keys || (rows > 0 && (!d_off || !d_adj || !d_rank || !d_keys)))
+    fail(GT_EINVAL, "null argument");
+  if (kbits < 1 || kbits > 31) fail(GT_EINVAL, "kbits must be in [1, 31]");
+  *m_keys = tc_orient_keys(d_off, d_adj, rows, row_lo, d_rank, kbits, d_keys);
+  GT_API_END
+}
+
+int gt_triangles_oriented_part(const int64_t* d_off_p, const int32_t* d_adj_p, int64_t n,
+                               int64_t m, int part, int nparts, int64_t* count) {
+  GT_API_BEGIN
+  if (!count) fail(GT_EINVAL, "count must not be NULL");
+  if (n > 0 && m > 0 && (!d_off_p || !d_adj_p)) fail(GT_EINVAL, "null argument");
+  *count = triangles_oriented(d_off_p, d_adj_p, n, m, part, nparts);
   GT_API_END
 }
 

@@ -15,9 +15,10 @@ GPUs of one box, NCCL over NVLink for the exchanges:
 * **PageRank** — 1D dst-range partition of the in-CSR; the contribution
   vector is replicated: every iteration all-gathers the owned slices and
   all-reduces the dangling mass (algorithms.py:72-85).
-* **Triangles** — the CSR shards are all-gathered (replicated CSR), every
-  rank counts an interleaved share of the work items, and the counts are
-  all-reduced (algorithms.py:110-118).
+* **Triangles** — the degree-ordered orientation is built sharded (each rank
+  symmetrises, ranks and orients its own rows; the oriented arcs are
+  all-gathered once), every rank counts the triangles of an interleaved share
+  of the middle vertices, and the counts are all-reduced (algorithms.py:98-118).
 
 All O(rows) / O(edges) work runs in libgtb200 kernels (``NativeOps``); this
 module only moves buffers and makes the O(ranks) decisions. ``ops`` is a
@@ -228,6 +229,48 @@ class NativeOps:
                                            int(last), score.data_ptr(), nxt.data_ptr(),
                                            part.data_ptr()), "gt_pagerank_step")
         return (score[:rows] if last else nxt[:rows]), part
+
+    def undirected_keys(self, off, adj, kbits, row_lo):
+        import ctypes
+
+        self._pre()
+        rows = off.numel() - 1
+        keys = self.empty(2 * adj.numel(), torch.int64)
+        n = ctypes.c_int64()
+        self._ck(self.lib.gt_tc_undirected_keys(off.data_ptr(), adj.data_ptr(), rows, row_lo, kbits,
+                                                keys.data_ptr(), ctypes.byref(n)),
+                 "gt_tc_undirected_keys")
+        return keys[:n.value]
+
+    def degree_rank(self, deg):
+        self._pre()
+        rank = self.empty(deg.numel(), torch.int32)
+        self._ck(self.lib.gt_tc_degree_rank(deg.data_ptr(), deg.numel(), rank.data_ptr()),
+                 "gt_tc_degree_rank")
+        return rank
+
+    def orient_keys(self, off, adj, row_lo, rank, kbits):
+        import ctypes
+
+        self._pre()
+        rows = off.numel() - 1
+        keys = self.empty(adj.numel(), torch.int64)
+        m = ctypes.c_int64()
+        self._ck(self.lib.gt_tc_orient_keys(off.data_ptr(), adj.data_ptr(), rows, row_lo,
+                                            rank.data_ptr(), kbits, keys.data_ptr(),
+                                            ctypes.byref(m)), "gt_tc_orient_keys")
+        return keys[:m.value]
+
+    def triangles_oriented_part(self, off_p, adj_p, part, nparts):
+        import ctypes
+
+        self._pre()
+        c = ctypes.c_int64()
+        self._ck(self.lib.gt_triangles_oriented_part(off_p.data_ptr(), adj_p.data_ptr(),
+                                                     off_p.numel() - 1, adj_p.numel(), part,
+                                                     nparts, ctypes.byref(c)),
+                 "gt_triangles_oriented_part")
+        return int(c.value)
 
     def triangles_part(self, graph, part, nparts):
         import ctypes
@@ -452,16 +495,58 @@ def pagerank(sg: ShardedGraph, damping: float = 0.85, iterations: int = 10, grou
 
 # --------------------------------------------------------------- triangles --
 
-def triangle_count(sg: ShardedGraph, group=None, ops=None, graph=None) -> int:
-    """Exact triangle count: replicated CSR, interleaved work split, all-reduce."""
+def orient(sg: ShardedGraph, group=None, ops=None):
+    """Degree-ordered orientation, sharded (algorithms.py:98-108): returns the
+    rank-space oriented CSR (off_p int64[n+1], adj_p int32[m]) replicated on
+    every rank. Each rank works on its own rows only:
+
+    1. both directions of its out-edges as undirected keys, sorted, deduped,
+       shuffled by first endpoint (the splitters as in build_csr) and merged:
+       rank r owns the undirected rows N(i) of an id range (graphs.py:163-167);
+    2. degrees all-gathered (n values), the (degree, id) rank computed on every
+       rank (one sort of n keys);
+    3. each rank orients its rows (arcs to higher-ranked neighbours), sorts
+       them, and ONE all-gather of the arcs plus a merge of the sorted runs
+       gives every rank the whole orientation — no replicated CSR pair and no
+       replicated orientation work."""
+    ops = ops or NativeOps()
+    world, rank = _world(group)
+    k = sg.kbits
+    sb, bucket_rows = _split_plan(sg.n, k)
+    und = ops.unique_keys(ops.sort_keys(ops.undirected_keys(sg.out_off, sg.out_adj, k,
+                                                             sg.out_bounds[rank]), 0, 2 * k))
+    counts = ops.bucket_counts(und, 2 * k - sb, 1 << sb)
+    dist.all_reduce(counts, group=group)
+    bounds = _range_bounds(counts.cpu().numpy(), world, sg.n, bucket_rows)
+    mine, sizes = _shuffle_by_rows(und, k, bounds, ops, group)
+    del und
+    mine = ops.unique_keys(ops.merge_runs(mine, sizes))
+    lo, hi = bounds[rank], bounds[rank + 1]
+    und_off, und_adj = ops.csr_from_keys(mine, k, lo, hi - lo)
+    del mine
+    rows = [bounds[r + 1] - bounds[r] for r in range(world)]
+    deg = _gather_known(und_off[1:] - und_off[:-1], rows, group)
+    rank_of = ops.degree_rank(deg)
+    arcs = ops.sort_keys(ops.orient_keys(und_off, und_adj, lo, rank_of, k), 0, 2 * k)
+    del und_off, und_adj
+    sizes_t = torch.tensor([arcs.numel()], dtype=torch.int64, device=arcs.device)
+    all_sizes = [torch.empty_like(sizes_t) for _ in range(world)]
+    dist.all_gather(all_sizes, sizes_t, group=group)
+    msizes = [int(x.item()) for x in all_sizes]
+    arcs = ops.merge_runs(_gather_known(arcs, msizes, group), msizes)
+    return ops.csr_from_keys(arcs, k, 0, sg.n)
+
+
+def triangle_count(sg: ShardedGraph, group=None, ops=None) -> int:
+    """Exact triangle count (algorithms.py:90-119): the sharded orientation
+    (`orient`), every rank counts the triangles whose middle vertex v is
+    rank (mod world) over the replicated N+ rows, one all-reduce."""
     if sg.n == 0 or sg.e == 0:
         return 0
     ops = ops or NativeOps()
     world, rank = _world(group)
-    if graph is None:
-        out_off, out_adj, in_off, in_adj = gather_csr(sg, group)
-        graph = ops.graph_from_csr(sg.n, sg.e, sg.ids, out_off, out_adj, in_off, in_adj)
-    c = torch.tensor([ops.triangles_part(graph, rank, world)], dtype=torch.int64,
-                     device=sg.ids.device)
+    off_p, adj_p = orient(sg, group, ops)
+    c = torch.tensor([ops.triangles_oriented_part(off_p, adj_p, rank, world)],
+                     dtype=torch.int64, device=sg.ids.device)
     dist.all_reduce(c, group=group)
     return int(c.item())

@@ -132,6 +132,40 @@ class CpuOps:
         part = torch.tensor([float(sc[inv == 0.0].sum())], dtype=torch.float64)
         return torch.from_numpy(sc if last else sc * inv), part
 
+    def undirected_keys(self, off, adj, kbits, row_lo):
+        o, a = off.numpy(), adj.numpy().astype(np.uint64)
+        u = (np.repeat(np.arange(o.size - 1), np.diff(o)) + row_lo).astype(np.uint64)
+        keep = a != u
+        u, a = u[keep], a[keep]
+        k = np.uint64(kbits)
+        return _t64(np.concatenate([(u << k) | a, (a << k) | u]))
+
+    def degree_rank(self, deg):
+        d = deg.numpy()
+        order = np.lexsort((np.arange(d.size), d))
+        rank = np.empty(d.size, dtype=np.int32)
+        rank[order] = np.arange(d.size, dtype=np.int32)
+        return torch.from_numpy(rank)
+
+    def orient_keys(self, off, adj, row_lo, rank, kbits):
+        o, a, r = off.numpy(), adj.numpy(), rank.numpy()
+        u = np.repeat(np.arange(o.size - 1), np.diff(o)) + row_lo
+        ru, rv = r[u].astype(np.uint64), r[a].astype(np.uint64)
+        keep = rv > ru
+        return _t64((ru[keep] << np.uint64(kbits)) | rv[keep])
+
+    def triangles_oriented_part(self, off_p, adj_p, part, nparts):
+        """sum over middle vertices v = part mod nparts of |N+(u) & N+(v)|, u in N-(v)."""
+        o, a = off_p.numpy(), adj_p.numpy()
+        n = o.size - 1
+        plus = [set(a[o[i]:o[i + 1]].tolist()) for i in range(n)]
+        total = 0
+        for u in range(n):
+            for v in a[o[u]:o[u + 1]].tolist():
+                if v % nparts == part:
+                    total += len(plus[u] & plus[v])
+        return total
+
     def triangles_part(self, graph, part, nparts):
         """v-centred count (u < v < w in (degree, id) rank) over v = part mod nparts."""
         n = graph["n"]

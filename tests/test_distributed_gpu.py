@@ -193,6 +193,54 @@ def test_triangle_parts_sum_to_total(native):
         assert sum(native.triangles_part(g, p, parts) for p in range(parts)) == total
 
 
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_sharded_orientation_primitives_match_cpu(native, world):
+    """The sharded orientation's per-rank primitives (undirected keys of a row
+    range, the (degree, id) rank, the oriented arcs of a row range, the count
+    over an orientation) against their CPU restatement, rank slices emulated
+    one after another; the parts sum to the single-GPU count."""
+    import paper_1503_07881_b200 as gt
+    from paper_1503_07881_b200.synth import rmat_edges
+
+    src, dst = rmat_edges(11, 30000, seed=12 + world, permute=True)
+    src = np.concatenate([src, src[:50]])  # self-loops and reciprocal pairs
+    dst = np.concatenate([dst, src[:50]])
+    want = ref.build_csr(src, dst, workers=1)
+    n, k, cpu = want.n, max(1, int(want.n - 1).bit_length()), CpuOps()
+    pos = {int(x): i for i, x in enumerate(want.ids)}
+    dense = np.array([pos[int(x)] for x in want.out_adj], dtype=np.int32)
+    cuts = [n * r // world for r in range(world + 1)]
+    und = []
+    for r in range(world):
+        a, b = cuts[r], cuts[r + 1]
+        off = torch.from_numpy(want.out_off[a:b + 1] - want.out_off[a])
+        adj = torch.from_numpy(dense[want.out_off[a]:want.out_off[b]])
+        got = native.undirected_keys(off.cuda(), adj.cuda(), k, a).cpu()
+        exp = cpu.undirected_keys(off, adj, k, a)
+        assert torch.equal(torch.sort(got).values, torch.sort(exp).values)
+        und.append(exp)
+    allk = torch.unique(torch.cat(und))
+    uoff, uadj = cpu.csr_from_keys(allk, k, 0, n)
+    deg = uoff[1:] - uoff[:-1]
+    rank = native.degree_rank(deg.cuda()).cpu()
+    assert torch.equal(rank, cpu.degree_rank(deg))
+    arcs = []
+    for r in range(world):
+        a, b = cuts[r], cuts[r + 1]
+        off = uoff[a:b + 1] - uoff[a]
+        adj = uadj[uoff[a]:uoff[b]]
+        got = native.orient_keys(off.cuda(), adj.cuda(), a, rank.cuda(), k).cpu()
+        assert torch.equal(got, cpu.orient_keys(off, adj, a, rank, k))
+        arcs.append(got)
+    off_p, adj_p = cpu.csr_from_keys(torch.sort(torch.cat(arcs)).values, k, 0, n)
+    g = gt.table_to_graph(gt.edge_table(src, dst), gt.EdgeSpec("src", "dst"))
+    total = gt.triangle_count(g)
+    parts = [native.triangles_oriented_part(off_p.cuda(), adj_p.cuda(), p, world)
+             for p in range(world)]
+    assert parts == [cpu.triangles_oriented_part(off_p, adj_p, p, world) for p in range(world)]
+    assert sum(parts) == total == ref.triangle_count_fast(want)
+
+
 def test_nccl_world1_pipeline_matches_oracle(native):
     import torch.distributed as dist
 
