@@ -1836,15 +1836,29 @@ static int64_t count_oriented(const Oriented& o, int part, int nparts) {
     // lists loaded into tables (4 B); hash tasks counted here too
     Phase ph("tc.count", 0.0);  // issue-bound probes: no HBM bytes claimed
     GT_CUDA(cudaMemsetAsync(counters + 22, 0, 4, s));
-    const int smem = 8 * gtd::TC_SLOTS * 4;
+    // GT_TC_WARPS (A/B): warps per CTA, each with its own 8 KB table; the
+    // grid fills every SM to its occupancy limit
+    static const int tc_warps = [] {
+      const char* env = getenv("GT_TC_WARPS");
+      const int w = env ? atoi(env) : 8;
+      return w < 1 ? 1 : (w > 8 ? 8 : w);
+    }();
+    const int smem = tc_warps * gtd::TC_SLOTS * 4;
     GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_warp_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_warp_kernel,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    int per_sm = 0;
+    GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gtd::tc_count_warp_kernel,
+                                                          32 * tc_warps, smem));
+    per_sm = std::max(per_sm, 1);
     // 16-bit copy of the window ranks for the bitmap tasks
     const int32_t base16 = int32_t(n - bm_bits);
     uint16_t* adj16 = reinterpret_cast<uint16_t*>(ws_get(WS_KEYS_A, size_t(m) * 2 + 64));
     if (n_bm) GT_LAUNCH(gtd::adj16_kernel, grid_cap(ceil_div64(m, 256)), 256, 0, o.adj_p, m, base16,
                         adj16);
-    GT_LAUNCH(gtd::tc_count_warp_kernel, ctx().sm_count * 3, 256, smem, o.off_p, o.adj_p, off_m,
+    GT_LAUNCH(gtd::tc_count_warp_kernel, ctx().sm_count * per_sm, 32 * tc_warps, smem, o.off_p,
+              o.adj_p, off_m,
               nm, tasks, n_bm, n_bm + n_sp, n_bm + n_wt, n, split_top, part, nparts, counters + 22,
               total, adj16, base16);
   }
