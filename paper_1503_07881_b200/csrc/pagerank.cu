@@ -979,7 +979,10 @@ static void pagerank_push(const gt_graph* g, double damping, int iterations, int
     double* cur = contrib[it & 1];
     double* nxt = contrib[(it + 1) & 1];
     {
-      Phase ph("pr.spmv", 12.0 * e + 8.0 * n * double(nbins));
+      // DRAM bytes: the keys (8 per edge), one forward sweep of contrib per
+      // bin; the reductions land in L2 (the accumulators' write-back is in
+      // pr.fixup's 32 bytes per node)
+      Phase ph("pr.spmv", 8.0 * e + 8.0 * n * double(nbins));
       for (int64_t b = 0; b < nbins; ++b) {
         const int64_t c = bs[size_t(b + 1)] - bs[size_t(b)];
         if (c > 0)
