@@ -122,7 +122,7 @@ def main():
     data = json.loads(path.read_text()) if path.exists() else {}
     c4 = {}
     m = {"build.minmax": "minmax_kernel", "build.presence": "presence_kernel",
-         "build.pack": "pack_kernel", "build.out_sort": "onesweep_kernel",
+         "build.pack": "pack_kernel", "build.out_sort": "onesweep",
          "build.dedupe": "segment_kernel", "pr.fixup": "pr_fixup_kernel"}
     for phase, k in m.items():
         hit = [v for kk, v in t.items() if kk.startswith(k)]
