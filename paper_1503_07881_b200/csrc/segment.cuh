@@ -13,7 +13,10 @@ namespace gtd {
 using gt::SortPlan;
 
 constexpr int SEG_KPT = 16;
-constexpr int SEG_MIN_CTAS = 4;  // resident CTAs per SM the register budget is sized for
+#ifndef GT_SEG_MIN_CTAS
+#define GT_SEG_MIN_CTAS 4
+#endif
+constexpr int SEG_MIN_CTAS = GT_SEG_MIN_CTAS;  // resident CTAs per SM the register budget is sized for
 constexpr int SEG_TILE = 256 * SEG_KPT;
 
 // Warp-cooperative fill of off[first..last] = v for the lanes that own a gap.
