@@ -1315,8 +1315,8 @@ void partition_pass(const uint64_t* in, uint64_t* out, int64_t n, int shift, int
                     const int64_t* d_digit_base) {
   cudaStream_t st = ctx().stream;
   const int nd = 1 << bits;
-  int64_t* d_seg = ws_n<int64_t>(WS_TMP3, 8);  // begin, end, tile offsets {0, tiles}
-  unsigned long long* d_cur = ws_n<unsigned long long>(WS_TMP4, size_t(nd));
+  int64_t* d_seg = ws_n<int64_t>(WS_PART, 8 + size_t(nd));  // begin, end, tile offsets {0, tiles}
+  unsigned long long* d_cur = reinterpret_cast<unsigned long long*>(d_seg + 8);
   const int64_t h_seg[4] = {0, n, 0, ceil_div64(n, PART_T)};
   h2d(d_seg, h_seg, sizeof h_seg);
   GT_CUDA(cudaMemcpyAsync(d_cur, d_digit_base, size_t(nd) * 8, cudaMemcpyDeviceToDevice, st));

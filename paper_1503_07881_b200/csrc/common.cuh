@@ -79,7 +79,9 @@ T* dalloc_n(size_t n) { return static_cast<T*>(dalloc(n * sizeof(T) + (n == 0 ? 
 // status words, histograms ...). Contents are undefined on return.
 enum Slot {
   WS_KEYS_A = 0, WS_KEYS_B, WS_LOOKBACK, WS_HIST, WS_COUNTERS, WS_SMALL,
-  WS_RANKMAP, WS_COLS, WS_TMP0, WS_TMP1, WS_TMP2, WS_TMP3, WS_TMP4, WS_NSLOTS
+  WS_RANKMAP, WS_COLS, WS_TMP0, WS_TMP1, WS_TMP2, WS_TMP3, WS_TMP4,
+  WS_PART,  // partition_pass's segment table and cursors (its callers own TMP0-4)
+  WS_NSLOTS
 };
 void* ws_get(Slot s, size_t bytes);
 template <typename T>

@@ -172,3 +172,4 @@ def test_push_within_destination_bins_matches_oracle(monkeypatch, bits):
     assert np.abs(push - pull).sum() <= 1e-12
     want = ref.pagerank_csr(ref.build_csr(src.astype(np.int64), dst.astype(np.int64)), 0.85, 20)
     assert np.abs(push - want).sum() <= L1_TOL
+
