@@ -1282,7 +1282,17 @@ __global__ void GT_TC_LB tc_count_warp_kernel(
 // allows (TC_CTA_SLOTS slots,
 // probed with shared-window loads: nearly every miss resolves in one probe),
 // or, when 2 d+(v) exceeds that, to a per-CTA global table of gtab_slots.
-constexpr int TC_CTA_SLOTS = 1 << 14;  // 64 KB: 3 CTAs per SM
+#ifndef GT_TC_CTA_LOG
+#define GT_TC_CTA_LOG 13
+#endif
+#ifndef GT_TC_CTA_MINB
+#define GT_TC_CTA_MINB 4
+#endif
+// 32 KB tables (bitmap window 2^18 ranks: 89 % of the CTA probes at C4; the
+// rest hashed), 4 CTAs per SM at 64 registers: C4 178 -> 161 ms against
+// 64 KB tables at 3 CTAs per SM (the kernel is latency-bound on its suffix
+// reads, so residency pays more than the wider bitmap window)
+constexpr int TC_CTA_SLOTS = 1 << GT_TC_CTA_LOG;
 
 struct SmemHashProbe {
   uint32_t stab;  // shared address of the slots
@@ -1300,9 +1310,9 @@ struct SmemHashProbe {
   }
 };
 
-// 3 CTAs per SM (the 64 KB table): with (256) alone ptxas settles on 48
-// registers and spills; (256, 3) gives 80, no spills (C4 182 -> 178 ms)
-__global__ void __launch_bounds__(256, 3) tc_count_cta_kernel(
+// with (256) alone ptxas settles on 48 registers and spills; the min-blocks
+// hint sizes the register budget to the residency the table allows
+__global__ void __launch_bounds__(256, GT_TC_CTA_MINB) tc_count_cta_kernel(
     const int64_t* __restrict__ off_p, const int32_t* __restrict__ adj_p,
     const int64_t* __restrict__ off_m, const int2* __restrict__ nm,
     const int2* __restrict__ tasks, int64_t n_tasks, int smem_log, int32_t* __restrict__ gtab,
@@ -1889,7 +1899,13 @@ static int64_t count_oriented(const Oriented& o, int part, int nparts) {
       const char* cw = getenv("GT_TC_CTA_WINDOW");
       cta_bm_bits = cw ? std::min<int64_t>(cta_bm_bits, atoll(cw)) : 0;
     }
-    const int grid = static_cast<int>(std::min<int64_t>(n_ct, 3LL * ctx().sm_count));
+    int per_sm = 0;
+    GT_CUDA(cudaFuncSetAttribute(gtd::tc_count_cta_kernel,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gtd::tc_count_cta_kernel, 256,
+                                                          smem));
+    const int grid = static_cast<int>(
+        std::min<int64_t>(n_ct, int64_t(std::max(per_sm, 1)) * ctx().sm_count));
     int32_t* gtab = nullptr;
     int gtab_log = 0;
     if (2 * max_dp > (int64_t(1) << smem_log)) {
