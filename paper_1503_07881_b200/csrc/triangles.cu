@@ -61,6 +61,17 @@ constexpr int TC_SPLIT_TOP = TC_BM_BITS / 2;   // split tables: bitmap of the to
 constexpr int TC_SPLIT_SLOTS = TC_SLOTS / 2;   // ... + hash of the rest (4 KB each)
 constexpr int TC_SPLIT_MAX = TC_SPLIT_SLOTS / 4;  // largest d+(v) of a split task
 constexpr int32_t TC_EMPTY = -1;
+// (register-budget knobs for sweeps: -DGT_PLACE_MINB=k / -DGT_FILL_MINB=k)
+#ifdef GT_PLACE_MINB
+#define GT_LB_PLACE __launch_bounds__(256, GT_PLACE_MINB)
+#else
+#define GT_LB_PLACE __launch_bounds__(256)
+#endif
+#ifdef GT_FILL_MINB
+#define GT_LB_FILL __launch_bounds__(256, GT_FILL_MINB)
+#else
+#define GT_LB_FILL __launch_bounds__(256)
+#endif
 
 __global__ void __launch_bounds__(256) cat_off_kernel(const int64_t* __restrict__ out_off,
                                                       const int64_t* __restrict__ in_off,
@@ -425,7 +436,7 @@ __device__ __forceinline__ int64_t shfl64(int64_t v, int src) {
 // by shuffle (measured faster than interleaving the rows across warps).
 // Rows with at most 32 candidates are packed several to a warp step (below);
 // longer rows take the warp one at a time.
-__global__ void __launch_bounds__(256) fill_rows_kernel(
+__global__ void GT_LB_FILL fill_rows_kernel(
     const int64_t* __restrict__ cat, const int64_t* __restrict__ out_off,
     const int32_t* __restrict__ out_adj, const int64_t* __restrict__ in_off,
     const int32_t* __restrict__ in_adj, int64_t n, const int32_t* __restrict__ rank,
@@ -730,7 +741,7 @@ __global__ void __launch_bounds__(256) place_rows_kernel(
 // handles 8 arcs and has all 8 N-(v) slot claims (returning atomics) in
 // flight at once, where the warp-per-row kernel waited on one claim per lane
 // per row (latency-bound: rows average ~30 arcs).
-__global__ void __launch_bounds__(256) place_tiles_kernel(
+__global__ void GT_LB_PLACE place_tiles_kernel(
     const int64_t* __restrict__ off_p, const int64_t* __restrict__ tile_row, int64_t m,
     const int32_t* __restrict__ order, const int64_t* __restrict__ und_off,
     const int32_t* __restrict__ buf, const int64_t* __restrict__ off_m,
