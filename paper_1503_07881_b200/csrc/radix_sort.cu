@@ -297,12 +297,16 @@ __device__ __forceinline__ uint32_t block_excl_scan_nt(uint32_t v, uint32_t* sm)
   return wpre + inc - v;
 }
 
+// Tiles are drawn in ticket order, so the tile `pf_dist` tickets ahead is one
+// that some CTA draws about one residency wave from now: its keys are pulled
+// into L2 here (cp.async.bulk.prefetch.L2), so that CTA's bulk copy finds them
+// there instead of waiting on DRAM. 0 = off.
 template <int BITS, int RS_MATCH, int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT)
     onesweep_smem_kernel(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int64_t n,
                          int shift, const int64_t* __restrict__ digit_base,
                          uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter,
-                         uint32_t epoch) {
+                         uint32_t epoch, int pf_dist) {
   constexpr int NW = NT / 32;
   constexpr int TILE = NT * RS_KPT;
   constexpr uint32_t mask = (1u << BITS) - 1u;
@@ -317,6 +321,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       bulk_load(s.keys, in + int64_t(t) * TILE, TILE * 8, &s.bar);
     }
+    if (pf_dist > 0 && int64_t(t + pf_dist + 1) * TILE <= n)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(in + int64_t(t + pf_dist) * TILE),
+                   "r"(TILE * 8)
+                   : "memory");
   }
   for (int i = tid; i < NW * 256; i += NT) (&s.whist[0][0])[i] = 0;
   __syncthreads();
@@ -517,8 +525,16 @@ static void launch_smem_bits(const uint64_t* src, uint64_t* dst, int64_t n, int 
     return true;
   }();
   (void)once;
+  // GT_SORT_PF: prefetch distance in tiles (default: one residency wave)
+  static const int pf_dist = [] {
+    const char* env = getenv("GT_SORT_PF");
+    if (env) return atoi(env);
+    int b = 0;
+    GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, NT, smem));
+    return b * ctx().sm_count;
+  }();
   GT_LAUNCH(kern, static_cast<int>(ceil_div64(n, int64_t(NT) * RS_KPT)), NT, smem, src, dst, n,
-            shift, digit_base, status, counter, epoch);
+            shift, digit_base, status, counter, epoch, pf_dist);
 }
 
 template <int NT>
