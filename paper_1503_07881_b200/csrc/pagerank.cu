@@ -131,8 +131,8 @@ __global__ void __launch_bounds__(256) pr_relabel_keys_kernel(const int64_t* __r
                                                               gt::SortPlan plan,
                                                               unsigned long long* __restrict__ hist,
                                                               uint64_t* __restrict__ keys) {
-  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
-  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * gt::RS_BINS];
+  for (int i = threadIdx.x; i < plan.passes * gt::RS_BINS; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
@@ -360,191 +360,6 @@ __global__ void __launch_bounds__(PR_THREADS, PR_MIN_BLOCKS) pr_spmv_kernel(
   pr_tile(int64_t(blockIdx.x), int(threadIdx.x), [] { __syncthreads(); }, vals, sr, in_off,
           in_adj, n, e, tile_row, contrib, inv_out, pos, base, damping, score, contrib_next, head,
           tail, tail_row, dpart, last_iter != 0, hot_bytes, total_bytes);
-}
-
-// ---- pipelined pull -----------------------------------------------------------
-// ncu of pr_spmv_kernel at C4 (profiles/r2s4_pr_probes.txt): no unit is
-// saturated (L1 data pipe 61 %, L2 53 %, DRAM 24 %, issue 43 %); the warps wait
-// on their gathers, and a CTA has gathers in flight for only part of a tile's
-// life (the tile_row -> in_off chain before them, the row sums after them).
-// This variant keeps them in flight all the time: a persistent CTA walks the
-// tiles c = blockIdx.x + k * gridDim.x with two shared-memory stages; the
-// gathers of a tile and its row metadata are issued as asynchronous copies
-// (cp.async: global -> shared, no register holds a value, no thread waits)
-// while the previous tile's rows are summed, and the edge indices and row
-// bounds of the tile after that are already on their way into registers. The
-// sums run in the same order as in pr_spmv_kernel: same bits.
-struct PrStage {
-  double vals[PR_TILE];
-  int64_t off[PR_ROWCAP + 2];   // raw in_off of rows r0 .. r0 + PR_ROWCAP + 1 (r0 = max(ra - 1, 0))
-  double inv[PR_ROWCAP + 1];
-  int32_t pos[PR_ROWCAP + 1];
-};
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                   uint32_t(__cvta_generic_to_shared(smem))), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async8_pol(void* smem, const void* g, uint64_t pol) {
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(
-                   uint32_t(__cvta_generic_to_shared(smem))), "l"(g), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                   uint32_t(__cvta_generic_to_shared(smem))), "l"(g) : "memory");
-}
-
-// Row sums of one staged tile (the counterpart of pr_rows + pr_finish over a
-// PrStage: offsets are raw in_off values, index r is relative to r0).
-__device__ __forceinline__ void pr_stage_rows(
-    const PrStage& S, int64_t c, int64_t ra, int64_t rb, const int64_t* __restrict__ in_off,
-    int64_t n, int64_t e, double base, double damping, const double* __restrict__ inv_out,
-    const int32_t* __restrict__ pos, double* __restrict__ score, double* __restrict__ contrib_next,
-    double* __restrict__ head, double* __restrict__ tail, int64_t* __restrict__ tail_row,
-    double* __restrict__ dpart, bool last_iter, int ltid) {
-  const int warp = ltid >> 5, lane = ltid & 31;
-  const int64_t e0 = c * PR_TILE;
-  const int64_t e1 = min(e, e0 + PR_TILE);
-  const int ne = e1 > e0 ? int(e1 - e0) : 0;
-  const int64_t r0 = ra > 0 ? ra - 1 : 0;
-  auto raw_off = [&](int64_t row) -> int64_t {  // in_off[row], staged when it is within the cap
-    const int64_t r = row - r0;
-    return r < PR_ROWCAP + 2 ? S.off[r] : in_off[row];
-  };
-  if (ltid == 0) tail_row[c] = -1;
-  const bool has_head = ne > 0 && (ra == n || raw_off(ra) > e0);
-  const int64_t first_row = has_head ? ra - 1 : ra;
-  const int64_t nseg = rb - first_row;
-  const bool has_tail = nseg > 0 && raw_off(rb) > e1 && !(has_head && nseg == 1);
-  auto off_at = [&](int64_t sgm) -> int {
-    const int64_t x = raw_off(first_row + sgm) - e0;
-    return int(x < 0 ? 0 : (x > ne ? ne : x));
-  };
-  double dang = 0.0;
-  auto finish = [&](int64_t sgm, double sum) {
-    const int64_t row = first_row + sgm;
-    if (has_head && sgm == 0) {
-      head[c] = sum;
-    } else if (has_tail && sgm == nseg - 1) {
-      tail[c] = sum;
-      tail_row[c] = row;
-    } else {
-      const double sc = base + damping * sum;
-      const int64_t r = row - r0;
-      const double inv = r < PR_ROWCAP + 1 ? S.inv[r] : inv_out[row];
-      if (!last_iter)
-        contrib_next[r < PR_ROWCAP + 1 ? int64_t(S.pos[r]) : (pos ? int64_t(pos[row]) : row)] = sc * inv;
-      else score[row] = sc;
-      if (inv == 0.0) dang += sc;
-    }
-  };
-  for (int64_t sgm = ltid; sgm < nseg; sgm += PR_THREADS) {  // short segments: thread per segment
-    const int a = off_at(sgm), b = off_at(sgm + 1);
-    if (b - a >= PR_LONG) continue;
-    double sum = 0.0;
-    for (int j = a; j < b; ++j) sum += S.vals[j];
-    finish(sgm, sum);
-  }
-  for (int64_t sgm = warp; sgm < nseg; sgm += PR_THREADS / 32) {  // long segments: warp per segment
-    const int a = off_at(sgm), b = off_at(sgm + 1);
-    if (b - a < PR_LONG) continue;  // warp-uniform
-    double sum = 0.0;
-    for (int j = a + lane; j < b; j += 32) sum += S.vals[j];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane == 0) finish(sgm, sum);
-  }
-  dang = warp_sum(dang);
-  if (lane == 0) dpart[c * (PR_THREADS / 32) + warp] = dang;
-}
-
-#ifndef GT_PR_PIPE_MINB
-#define GT_PR_PIPE_MINB 4
-#endif
-__global__ void __launch_bounds__(PR_THREADS, GT_PR_PIPE_MINB) pr_spmv_pipe_kernel(
-    const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_adj, int64_t n, int64_t e,
-    int64_t n_total, const int64_t* __restrict__ tile_row, const double* __restrict__ contrib,
-    const double* __restrict__ inv_out, const int32_t* __restrict__ pos,
-    const double* __restrict__ dangling_prev, double damping,
-    double* __restrict__ score, double* __restrict__ contrib_next, double* __restrict__ head,
-    double* __restrict__ tail, int64_t* __restrict__ tail_row, double* __restrict__ dpart,
-    int last_iter, uint32_t hot_bytes, uint32_t total_bytes, int64_t tiles) {
-  extern __shared__ __align__(16) unsigned char pr_dsm[];
-  PrStage* st = reinterpret_cast<PrStage*>(pr_dsm);  // [2]
-  constexpr int PER = PR_TILE / PR_THREADS;
-  const int tid = threadIdx.x;
-  const double base =
-      (1.0 - damping) / double(n_total) + damping * (*dangling_prev / double(n_total));
-  uint64_t pol = 0;
-  if (hot_bytes)
-    asm volatile("createpolicy.range.global.L2::evict_last.L2::evict_first.b64 %0, [%1], %2, %3;"
-                 : "=l"(pol) : "l"(contrib), "r"(hot_bytes), "r"(total_bytes));
-  const int64_t G = gridDim.x;
-  // registers of the tile that is issued next: its edge indices and row bounds
-  int32_t idx[PER];
-  int64_t ra = 0, rb = 0;
-  auto load_meta = [&](int64_t t) {
-    const int64_t e0 = t * PR_TILE;
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int64_t j = e0 + i * PR_THREADS + tid;
-      idx[i] = j < e ? __ldcs(in_adj + j) : -1;
-    }
-    ra = tile_row[t];
-    rb = tile_row[t + 1];
-  };
-  auto issue = [&](int64_t t, PrStage& S) {  // asynchronous: gathers + row metadata of tile t
-    if (hot_bytes) {
-#pragma unroll
-      for (int i = 0; i < PER; ++i)
-        if (idx[i] >= 0) cp_async8_pol(&S.vals[i * PR_THREADS + tid], contrib + idx[i], pol);
-    } else {
-#pragma unroll
-      for (int i = 0; i < PER; ++i)
-        if (idx[i] >= 0) cp_async8(&S.vals[i * PR_THREADS + tid], contrib + idx[i]);
-    }
-    const int64_t r0 = ra > 0 ? ra - 1 : 0;
-    const int64_t nst = min(rb - r0 + 1, int64_t(PR_ROWCAP + 2));  // rows r0 .. rb
-    for (int64_t r = tid; r < nst; r += PR_THREADS) {
-      const int64_t row = r0 + r;
-      cp_async8(&S.off[r], in_off + row);
-      if (row < n && r < PR_ROWCAP + 1) {
-        cp_async8(&S.inv[r], inv_out + row);
-        if (pos) cp_async4(&S.pos[r], pos + row);
-        else S.pos[r] = int32_t(row);
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-
-  int64_t t_issue = blockIdx.x;
-  if (t_issue >= tiles) return;
-  load_meta(t_issue);
-  int64_t pend = t_issue, pend_ra = ra, pend_rb = rb;
-  issue(t_issue, st[0]);
-  t_issue += G;
-  if (t_issue < tiles) load_meta(t_issue);
-  int buf = 0;
-  while (pend >= 0) {
-    const int64_t cur = pend, cur_ra = pend_ra, cur_rb = pend_rb;
-    if (t_issue < tiles) {
-      pend = t_issue;
-      pend_ra = ra;
-      pend_rb = rb;
-      issue(t_issue, st[buf ^ 1]);
-      t_issue += G;
-      if (t_issue < tiles) load_meta(t_issue);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");  // all but the newest group: tile cur landed
-    } else {
-      pend = -1;
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    pr_stage_rows(st[buf], cur, cur_ra, cur_rb, in_off, n, e, base, damping, inv_out, pos, score,
-                  contrib_next, head, tail, tail_row, dpart, last_iter != 0, tid);
-    __syncthreads();  // the stage is free again
-    buf ^= 1;
-  }
 }
 
 __global__ void __launch_bounds__(256) pr_fixup_kernel(
@@ -926,8 +741,8 @@ __global__ void __launch_bounds__(256) pr_push_keys_kernel(const int64_t* __rest
                                                            int64_t n, int kbits, gt::SortPlan plan,
                                                            unsigned long long* __restrict__ hist,
                                                            uint64_t* __restrict__ keys) {
-  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
-  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * gt::RS_BINS];
+  for (int i = threadIdx.x; i < plan.passes * gt::RS_BINS; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t nw = int64_t(gridDim.x) * 8;
@@ -1354,22 +1169,6 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
     sync();
     return;
   }
-  // GT_PR_PIPE=1: the pipelined persistent kernel (grid = resident CTAs)
-  static const int pipe_grid = [] {
-    const char* env = getenv("GT_PR_PIPE");
-    if (!env || atoi(env) <= 0) return 0;
-    const size_t dyn = 2 * sizeof(gtd::PrStage);
-    GT_CUDA(cudaFuncSetAttribute(gtd::pr_spmv_pipe_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn)));
-    GT_CUDA(cudaFuncSetAttribute(gtd::pr_spmv_pipe_kernel,
-                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    int b = 0;
-    GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, gtd::pr_spmv_pipe_kernel,
-                                                          gtd::PR_THREADS, dyn));
-    if (getenv("GT_PR_DEBUG"))
-      fprintf(stderr, "[gt pr] pipelined spmv: %d CTAs/SM, %zu B smem\n", b, dyn);
-    return std::max(1, b) * ctx().sm_count;
-  }();
   static const int pf_dist = [] {  // GT_PR_PF: index prefetch distance in tiles (0 = off)
     const char* env = getenv("GT_PR_PF");  // measured at C4: 0 / 444 / 888 tiles within 0.5 %
     return env ? atoi(env) : 0;
@@ -1380,15 +1179,9 @@ void pagerank(const gt_graph* g, double damping, int iterations, double* scores,
     double* nxt = contrib[(it + 1) & 1];
     {
       Phase ph("pr.spmv", 12.0 * e + 8.0 * (n + 1) + 20.0 * n);
-      if (pipe_grid)
-        GT_LAUNCH(gtd::pr_spmv_pipe_kernel, int(std::min<int64_t>(tiles, pipe_grid)),
-                  gtd::PR_THREADS, 2 * sizeof(gtd::PrStage), g->in_off, in_adj_r, n, e, n, tile_row,
-                  cur, inv_out, pos, dang + it, damping, score, nxt, head, tail, tail_row, dpart,
-                  last, hot_bytes, total_bytes, tiles);
-      else
-        GT_LAUNCH(gtd::pr_spmv_kernel, static_cast<int>(tiles), gtd::PR_THREADS, 0, g->in_off,
-                  in_adj_r, n, e, n, tile_row, cur, inv_out, pos, dang + it, damping, score, nxt,
-                  head, tail, tail_row, dpart, last, hot_bytes, total_bytes, pf_dist);
+      GT_LAUNCH(gtd::pr_spmv_kernel, static_cast<int>(tiles), gtd::PR_THREADS, 0, g->in_off,
+                in_adj_r, n, e, n, tile_row, cur, inv_out, pos, dang + it, damping, score, nxt,
+                head, tail, tail_row, dpart, last, hot_bytes, total_bytes, pf_dist);
     }
     {
       Phase ph("pr.fixup", 40.0 * tiles);
