@@ -173,8 +173,8 @@ __global__ void __launch_bounds__(256) pack_kernel(const int64_t* __restrict__ s
                                                    int kbits, SortPlan plan,
                                                    unsigned long long* __restrict__ hist,
                                                    uint64_t* __restrict__ keys) {
-  __shared__ uint32_t sh[gt::RS_MAX_PASSES * gt::RS_BINS];
-  for (int i = threadIdx.x; i < plan.passes * gt::RS_BINS; i += blockDim.x) sh[i] = 0;
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
+  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   // U rows per thread per step: all 2U column loads, then all 2U rank
   // lookups, are in flight before the first key is formed (the single-row
@@ -231,8 +231,8 @@ __global__ void __launch_bounds__(256) idkeys_kernel(const int64_t* __restrict__
                                                      int64_t lo, SortPlan plan,
                                                      unsigned long long* __restrict__ hist,
                                                      uint64_t* __restrict__ keys) {
-  __shared__ uint32_t sh[gt::RS_MAX_PASSES * gt::RS_BINS];
-  for (int i = threadIdx.x; i < plan.passes * gt::RS_BINS; i += blockDim.x) sh[i] = 0;
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
+  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -353,10 +353,10 @@ __global__ void __launch_bounds__(256) dedupe_count_kernel(const uint64_t* __res
                                                            int64_t n, int kbits, SortPlan in_plan,
                                                            unsigned long long* __restrict__ dup_hist,
                                                            int64_t* __restrict__ tile_cnt) {
-  __shared__ uint32_t sh[gt::RS_MAX_PASSES * gt::RS_BINS];
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
   __shared__ uint32_t s_w[8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < in_plan.passes * gt::RS_BINS; i += 256) sh[i] = 0;
+  for (int i = tid; i < in_plan.passes * 256; i += 256) sh[i] = 0;
   __syncthreads();
   const int64_t wbase = int64_t(blockIdx.x) * SEG_TILE + int64_t(warp) * 32 * SEG_KPT;
   const uint64_t lowmask = (1ull << kbits) - 1ull;
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(256) dedupe_count_kernel(const uint64_t* __res
 #pragma unroll
       for (int q = 0; q < gt::RS_MAX_PASSES; ++q)
         if (q < in_plan.passes)
-          atomicAdd(&sh[q * gt::RS_BINS + (uint32_t(ik >> in_plan.shift[q]) & ((1u << in_plan.bits[q]) - 1u))],
+          atomicAdd(&sh[q * 256 + (uint32_t(ik >> in_plan.shift[q]) & ((1u << in_plan.bits[q]) - 1u))],
                     cnt);
     }
   }
@@ -417,16 +417,14 @@ __global__ void __launch_bounds__(256) in_hist_kernel(const unsigned long long* 
   const int b = in_plan.bits[q];
   const int p = src_pass.shift[q];  // the out pass holding in-digit q (low bits of its digit)
   const int w = src_pass.bits[q];   // that out digit's width
-  for (uint32_t x = threadIdx.x; x < uint32_t(gt::RS_BINS); x += blockDim.x) {
-    if (x >= (1u << b)) {
-      in_hist[q * gt::RS_BINS + x] = 0;
-      continue;
-    }
-    unsigned long long c = 0;
-    for (uint32_t hi = 0; hi < (1u << (w - b)); ++hi)
-      c += out_hist[p * gt::RS_BINS + (hi << b | x)];
-    in_hist[q * gt::RS_BINS + x] = c - dup_hist[q * gt::RS_BINS + x];
+  const uint32_t x = threadIdx.x;
+  if (x >= (1u << b)) {
+    if (x < 256) in_hist[q * 256 + x] = 0;
+    return;
   }
+  unsigned long long c = 0;
+  for (uint32_t hi = 0; hi < (1u << (w - b)); ++hi) c += out_hist[p * 256 + (hi << b | x)];
+  in_hist[q * 256 + x] = c - dup_hist[q * 256 + x];
 }
 
 }  // namespace gtd
@@ -438,33 +436,21 @@ namespace gt {
 // then the rest of the src bits. The in-sort digits are the out digits cut to
 // the dst bits (in_hist_kernel), so this keeps them near-equal too (C4: out
 // 7,7,6,8,8,8,8 -> in 7,7,6,6) without adding a pass over make_plan.
-// mb = widest digit: 8, or 9 (GT_SORT_BITS, the default) which takes the C4
-// sorts from 7 + 4 to 6 + 3 passes (out 9,9,9,9,8,8 -> in 9,9,8).
-static int build_digit_bits() {
-  static const int mb = [] {
-    const char* env = getenv("GT_SORT_BITS");
-    const int v = env ? atoi(env) : 9;
-    return v >= 9 ? 9 : 8;
-  }();
-  return mb;
-}
-
 static SortPlan make_out_plan(int kb) {
-  const int mb = build_digit_bits();
-  SortPlan full = make_plan(0, 2 * kb, mb);
+  SortPlan full = make_plan(0, 2 * kb);
   if (kb <= 0) return full;
   SortPlan p;
-  const int nd = (kb + mb - 1) / mb;
+  const int nd = (kb + 7) / 8;
   int shift = 0;
   for (int q = 0; q < nd; ++q) {
     int b = kb / nd + (q < kb % nd ? 1 : 0);
-    if (q == nd - 1) b = std::min(mb, 2 * kb - shift);
+    if (q == nd - 1) b = std::min(8, 2 * kb - shift);
     p.shift[p.passes] = shift;
     p.bits[p.passes++] = b;
     shift += b;
   }
   const int rest = 2 * kb - shift;
-  const int nr = (rest + mb - 1) / mb;
+  const int nr = (rest + 7) / 8;
   for (int q = 0; q < nr; ++q) {
     const int b = rest / nr + (q < rest % nr ? 1 : 0);
     p.shift[p.passes] = shift;
@@ -685,8 +671,8 @@ gt_graph* build_csr(const int64_t* src, const int64_t* dst, int64_t rows, const 
       Phase ph("build.dedupe", 16.0 * rows);
       const int64_t tiles = ceil_div64(rows, gtd::SEG_TILE);
       int64_t* tile_base = ws_n<int64_t>(WS_TMP3, size_t(tiles) + 1);
-      unsigned long long* dup = ws_n<unsigned long long>(WS_TMP4, RS_MAX_PASSES * RS_BINS);
-      GT_CUDA(cudaMemsetAsync(dup, 0, RS_MAX_PASSES * RS_BINS * 8, s));
+      unsigned long long* dup = ws_n<unsigned long long>(WS_TMP4, RS_MAX_PASSES * 256);
+      GT_CUDA(cudaMemsetAsync(dup, 0, RS_MAX_PASSES * 256 * 8, s));
       GT_LAUNCH(gtd::dedupe_count_kernel, static_cast<int>(tiles), 256, 0, sorted, rows, kb_bits,
                 in_plan, dup, tile_base);
       exclusive_scan_i64(tile_base, tiles, small + 3);

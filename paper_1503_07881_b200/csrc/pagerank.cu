@@ -131,8 +131,8 @@ __global__ void __launch_bounds__(256) pr_relabel_keys_kernel(const int64_t* __r
                                                               gt::SortPlan plan,
                                                               unsigned long long* __restrict__ hist,
                                                               uint64_t* __restrict__ keys) {
-  __shared__ uint32_t sh[gt::RS_MAX_PASSES * gt::RS_BINS];
-  for (int i = threadIdx.x; i < plan.passes * gt::RS_BINS; i += blockDim.x) sh[i] = 0;
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
+  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
@@ -741,8 +741,8 @@ __global__ void __launch_bounds__(256) pr_push_keys_kernel(const int64_t* __rest
                                                            int64_t n, int kbits, gt::SortPlan plan,
                                                            unsigned long long* __restrict__ hist,
                                                            uint64_t* __restrict__ keys) {
-  __shared__ uint32_t sh[gt::RS_MAX_PASSES * gt::RS_BINS];
-  for (int i = threadIdx.x; i < plan.passes * gt::RS_BINS; i += blockDim.x) sh[i] = 0;
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
+  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t nw = int64_t(gridDim.x) * 8;

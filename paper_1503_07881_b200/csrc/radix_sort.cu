@@ -22,8 +22,8 @@ constexpr int LB_WIN = GT_LB_WIN;
 __global__ void __launch_bounds__(256) hist_kernel(const uint64_t* __restrict__ keys, int64_t n,
                                                    gt::SortPlan plan,
                                                    unsigned long long* __restrict__ ghist) {
-  __shared__ uint32_t sh[gt::RS_MAX_PASSES * gt::RS_BINS];
-  for (int i = threadIdx.x; i < plan.passes * gt::RS_BINS; i += blockDim.x) sh[i] = 0;
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
+  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -32,19 +32,15 @@ __global__ void __launch_bounds__(256) hist_kernel(const uint64_t* __restrict__ 
   plan_hist_flush(sh, plan, ghist);
 }
 
-// grid = passes, block = 256: exclusive scan of each pass's RS_BINS digit
-// counts (two consecutive digits per thread).
+// grid = passes, block = 256: exclusive scan of each pass's 256 digit counts.
 __global__ void __launch_bounds__(256) digit_scan_kernel(const unsigned long long* __restrict__ ghist,
                                                          int64_t* __restrict__ base) {
-  static_assert(gt::RS_BINS == 512, "two digits per thread");
   __shared__ int64_t sm[8];
   const int q = blockIdx.x;
-  const int64_t a = int64_t(ghist[q * gt::RS_BINS + 2 * threadIdx.x]);
-  const int64_t b = int64_t(ghist[q * gt::RS_BINS + 2 * threadIdx.x + 1]);
+  int64_t v = int64_t(ghist[q * 256 + threadIdx.x]);
   int64_t tot;
-  const int64_t ex = block_excl_scan_256<int64_t>(a + b, sm, tot);
-  base[q * gt::RS_BINS + 2 * threadIdx.x] = ex;
-  base[q * gt::RS_BINS + 2 * threadIdx.x + 1] = ex + a;
+  int64_t ex = block_excl_scan_256<int64_t>(v, sm, tot);
+  base[q * 256 + threadIdx.x] = ex;
 }
 
 // One onesweep LSD pass over a BITS-wide digit (BITS is a template parameter
@@ -248,11 +244,11 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MIN_BLOCKS)
 #endif
 constexpr int SMEM_LB_WIN = GT_SMEM_LB_WIN;
 
-template <int NT, int BINS>
+template <int NT>
 struct OnesweepSmemT {
   uint64_t keys[NT * RS_KPT];  // the tile by index, then scattered in place by position
-  uint32_t whist[NT / 32][BINS];
-  int64_t gbase[BINS];
+  uint32_t whist[NT / 32][256];
+  int64_t gbase[256];
   unsigned long long bar;
   uint32_t scan[NT / 32];
   int tile;
@@ -314,10 +310,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
   constexpr int NW = NT / 32;
   constexpr int TILE = NT * RS_KPT;
   constexpr uint32_t mask = (1u << BITS) - 1u;
-  constexpr int BINS = BITS > 8 ? 512 : 256;         // histogram slots (and status stride)
-  constexpr int DPT = (1 << BITS) > NT ? (1 << BITS) / NT : 1;  // digits per thread (consecutive)
   extern __shared__ __align__(128) unsigned char os1_dsm[];
-  OnesweepSmemT<NT, BINS>& s = *reinterpret_cast<OnesweepSmemT<NT, BINS>*>(os1_dsm);
+  OnesweepSmemT<NT>& s = *reinterpret_cast<OnesweepSmemT<NT>*>(os1_dsm);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     const int t = int(atomicAdd(tile_counter, 1u));
@@ -332,7 +326,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
                    "r"(TILE * 8)
                    : "memory");
   }
-  for (int i = tid; i < NW * BINS; i += NT) (&s.whist[0][0])[i] = 0;
+  for (int i = tid; i < NW * 256; i += NT) (&s.whist[0][0])[i] = 0;
   __syncthreads();
   const int cur = s.tile;
   const int64_t base = int64_t(cur) * TILE;
@@ -386,81 +380,49 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
   }
   __syncthreads();
 
-  // per digit (thread tid owns digits tid*DPT .. tid*DPT+DPT-1): warp offsets,
-  // tile count, decoupled look-back (the digits of a thread polled together)
-  uint32_t tile_cnt[DPT];
-  {
-    uint64_t excl[DPT];
-    int t[DPT];
-    bool done[DPT];
+  uint32_t tile_cnt = 0;
+  if (tid < (1 << BITS)) {  // per digit: warp offsets, tile count, decoupled look-back
+    const int d = tid;
 #pragma unroll
-    for (int j = 0; j < DPT; ++j) {
-      const int d = tid * DPT + j;
-      tile_cnt[j] = 0;
-      excl[j] = 0;
-      t[j] = cur - 1;
-      done[j] = d >= (1 << BITS) || cur == 0;
-      if (d < (1 << BITS)) {
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-          const uint32_t c = s.whist[w][d];
-          s.whist[w][d] = tile_cnt[j];
-          tile_cnt[j] += c;
-        }
-        st_status_u64(status + int64_t(cur) * BINS + d,
-                      lb_pack(cur == 0 ? LB_INC : LB_AGG, epoch, tile_cnt[j]));
-      }
+    for (int w = 0; w < NW; ++w) {
+      const uint32_t c = s.whist[w][d];
+      s.whist[w][d] = tile_cnt;
+      tile_cnt += c;
     }
-    const uint64_t ep = uint64_t(epoch & 0x3FFFFFu);
-    bool all = false;
-    while (!all) {
-      all = true;
-#pragma unroll
-      for (int j = 0; j < DPT; ++j) {
-        if (done[j]) continue;
-        const int d = tid * DPT + j;
+    uint64_t* st = status + int64_t(cur) * 256 + d;
+    st_status_u64(st, lb_pack(cur == 0 ? LB_INC : LB_AGG, epoch, tile_cnt));
+    uint64_t excl = 0;
+    if (cur > 0) {
+      const uint64_t ep = uint64_t(epoch & 0x3FFFFFu);
+      int t = cur - 1;
+      bool done = false;
+      while (!done) {
         uint64_t v[SMEM_LB_WIN];
 #pragma unroll
         for (int q = 0; q < SMEM_LB_WIN; ++q)
-          v[q] = t[j] - q >= 0 ? ld_status_u64(status + int64_t(t[j] - q) * BINS + d) : 0ull;
+          v[q] = t - q >= 0 ? ld_status_u64(status + int64_t(t - q) * 256 + d) : 0ull;
 #pragma unroll
         for (int q = 0; q < SMEM_LB_WIN; ++q) {
-          if (done[j] || t[j] < 0) break;
+          if (done || t < 0) break;
           if (((v[q] >> 40) & 0x3FFFFFu) != ep || (v[q] >> 62) == 0) break;  // re-poll
-          excl[j] += v[q] & ((1ull << 40) - 1);
-          if ((v[q] >> 62) == 2) done[j] = true;
-          else --t[j];
+          excl += v[q] & ((1ull << 40) - 1);
+          if ((v[q] >> 62) == 2) done = true;
+          else --t;
         }
-        if (!done[j]) all = false;
       }
+      st_status_u64(st, lb_pack(LB_INC, epoch, excl + tile_cnt));
     }
-#pragma unroll
-    for (int j = 0; j < DPT; ++j) {
-      const int d = tid * DPT + j;
-      if (d < (1 << BITS)) {
-        if (cur > 0)
-          st_status_u64(status + int64_t(cur) * BINS + d, lb_pack(LB_INC, epoch, excl[j] + tile_cnt[j]));
-        s.gbase[d] = digit_base[d] + int64_t(excl[j]);
-      }
-    }
+    s.gbase[d] = digit_base[d] + int64_t(excl);
   }
 #ifdef GT_SMEM_LB_SYNC
   __syncthreads();
 #endif
   {  // in-tile digit starts (exclusive scan of the tile counts over the digits)
-    uint32_t mine = 0;
+    const uint32_t start = block_excl_scan_nt<NT>(tile_cnt, s.scan);
+    if (tid < (1 << BITS)) {
+      s.gbase[tid] -= int64_t(start);
 #pragma unroll
-    for (int j = 0; j < DPT; ++j) mine += tile_cnt[j];
-    uint32_t start = block_excl_scan_nt<NT>(mine, s.scan);
-#pragma unroll
-    for (int j = 0; j < DPT; ++j) {
-      const int d = tid * DPT + j;
-      if (d < (1 << BITS)) {
-        s.gbase[d] -= int64_t(start);
-#pragma unroll
-        for (int w = 0; w < NW; ++w) s.whist[w][d] += start;
-      }
-      start += tile_cnt[j];
+      for (int w = 0; w < NW; ++w) s.whist[w][tid] += start;
     }
   }
   __syncthreads();
@@ -497,12 +459,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
 
 namespace gt {
 
-SortPlan make_plan(int lo_bit, int hi_bit, int max_bits) {
+SortPlan make_plan(int lo_bit, int hi_bit) {
   SortPlan p;
   int width = hi_bit - lo_bit;
   if (width <= 0) return p;
-  max_bits = max_bits >= 9 ? 9 : 8;
-  p.passes = (width + max_bits - 1) / max_bits;
+  p.passes = (width + 7) / 8;
   int shift = lo_bit;
   for (int q = 0; q < p.passes; ++q) {
     int b = width / p.passes + (q < width % p.passes ? 1 : 0);
@@ -514,12 +475,12 @@ SortPlan make_plan(int lo_bit, int hi_bit, int max_bits) {
 }
 
 SortHist sort_hist_begin(int slot_index) {
-  char* base = static_cast<char*>(ws_get(WS_HIST, 2 * (RS_MAX_PASSES * RS_BINS * 16)));
-  base += slot_index * (RS_MAX_PASSES * RS_BINS * 16);
+  char* base = static_cast<char*>(ws_get(WS_HIST, 2 * (RS_MAX_PASSES * 256 * 16)));
+  base += slot_index * (RS_MAX_PASSES * 256 * 16);
   SortHist h;
   h.hist = reinterpret_cast<unsigned long long*>(base);
-  h.digit_base = reinterpret_cast<int64_t*>(base + RS_MAX_PASSES * RS_BINS * 8);
-  GT_CUDA(cudaMemsetAsync(h.hist, 0, RS_MAX_PASSES * RS_BINS * 8, ctx().stream));
+  h.digit_base = reinterpret_cast<int64_t*>(base + RS_MAX_PASSES * 256 * 8);
+  GT_CUDA(cudaMemsetAsync(h.hist, 0, RS_MAX_PASSES * 256 * 8, ctx().stream));
   return h;
 }
 
@@ -552,7 +513,7 @@ static void launch_smem_bits(const uint64_t* src, uint64_t* dst, int64_t n, int 
                              const int64_t* digit_base, uint64_t* status, uint32_t* counter,
                              uint32_t epoch) {
   constexpr auto kern = gtd::onesweep_smem_kernel<BITS, M, NT>;
-  constexpr size_t smem = sizeof(gtd::OnesweepSmemT<NT, (BITS > 8 ? 512 : 256)>);
+  constexpr size_t smem = sizeof(gtd::OnesweepSmemT<NT>);
   static const bool once = [] {  // thread-safe one-time set-up
     GT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     GT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -586,9 +547,9 @@ static void launch_smem(int bits, const uint64_t* src, uint64_t* dst, int64_t n,
     launch_smem_bits<B, 6, NT>(src, dst, n, shift, digit_base, status, counter, epoch);      \
     break;
     GT_SMEM_CASE(1) GT_SMEM_CASE(2) GT_SMEM_CASE(3) GT_SMEM_CASE(4)
-    GT_SMEM_CASE(5) GT_SMEM_CASE(6) GT_SMEM_CASE(7) GT_SMEM_CASE(8) GT_SMEM_CASE(9)
+    GT_SMEM_CASE(5) GT_SMEM_CASE(6) GT_SMEM_CASE(7) GT_SMEM_CASE(8)
 #undef GT_SMEM_CASE
-    default: fail(GT_EINVAL, "radix digit width must be 1..9");
+    default: fail(GT_EINVAL, "radix digit width must be 1..8");
   }
 }
 
@@ -619,8 +580,6 @@ static void launch_onesweep(int bits, int nmatch, int grid, const uint64_t* src,
     const char* env = getenv("GT_SORT_KERNEL");
     return env ? atoi(env) : 1;
   }();
-  if (bits > 8 && (kind <= 0 || (reinterpret_cast<uintptr_t>(src) & 15u) != 0))
-    fail(GT_EINVAL, "9-bit radix digits need the shared-memory pass and 16-byte aligned keys");
   if (kind > 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
     if (kind == 2) launch_smem<512>(bits, src, dst, n, shift, digit_base, status, counter, epoch);
     else launch_smem<256>(bits, src, dst, n, shift, digit_base, status, counter, epoch);
@@ -643,9 +602,7 @@ uint64_t* radix_sort(uint64_t* a, uint64_t* b, int64_t n, const SortPlan& plan, 
   if (n <= 1 || plan.passes == 0) return a;
   const int64_t tiles = ceil_div64(n, RS_TILE);
   if (tiles >= (1ll << 31)) fail(GT_ECAPACITY, "radix sort: too many tiles");
-  int widest = 8;
-  for (int q = 0; q < plan.passes; ++q) widest = std::max(widest, plan.bits[q]);
-  uint64_t* status = ws_n<uint64_t>(WS_LOOKBACK, size_t(tiles) << widest);
+  uint64_t* status = ws_n<uint64_t>(WS_LOOKBACK, size_t(tiles) * 256);
   uint32_t* counters = ws_n<uint32_t>(WS_COUNTERS, 64);
   GT_CUDA(cudaMemsetAsync(counters, 0, RS_MAX_PASSES * sizeof(uint32_t), ctx().stream));
   {
@@ -665,13 +622,13 @@ uint64_t* radix_sort(uint64_t* a, uint64_t* b, int64_t n, const SortPlan& plan, 
   for (int q = 0; q < plan.passes; ++q) {
     Phase ph(phase, 16.0 * n);
     if (q == 0 && first_unstable && !stable_only) {
-      partition_pass(src, dst, n, plan.shift[q], plan.bits[q], h.digit_base + q * RS_BINS);
+      partition_pass(src, dst, n, plan.shift[q], plan.bits[q], h.digit_base + q * 256);
       std::swap(src, dst);
       continue;
     }
     const uint32_t epoch = next_epoch();
     launch_onesweep(plan.bits[q], nmatch, static_cast<int>(tiles), src, dst, n, plan.shift[q],
-                    h.digit_base + q * RS_BINS, status, counters + q, epoch);
+                    h.digit_base + q * 256, status, counters + q, epoch);
     std::swap(src, dst);
   }
   return src;

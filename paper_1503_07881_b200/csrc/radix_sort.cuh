@@ -21,7 +21,6 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_KPT = 16;
 constexpr int RS_TILE = RS_THREADS * RS_KPT;  // 4096 keys
 constexpr int RS_MAX_PASSES = 8;
-constexpr int RS_BINS = 512;  // histogram slots per pass: digits are at most 9 bits wide
 
 struct SortPlan {
   int passes = 0;
@@ -29,11 +28,10 @@ struct SortPlan {
   int bits[RS_MAX_PASSES] = {0};
 };
 
-// Split [lo_bit, hi_bit) into ceil(width/max_bits) near-equal digits, LSD first
-// (max_bits 8, or 9 for the two big sorts of the build: fewer passes).
-SortPlan make_plan(int lo_bit, int hi_bit, int max_bits = 8);
+// Split [lo_bit, hi_bit) into ceil(width/8) near-equal digits, LSD first.
+SortPlan make_plan(int lo_bit, int hi_bit);
 
-// Device scratch for a sort: histograms [passes][RS_BINS] (u64), digit bases.
+// Device scratch for a sort: histograms [passes][256] (u64), digit bases.
 struct SortHist {
   unsigned long long* hist;  // zeroed by sort_hist_begin
   int64_t* digit_base;
@@ -127,20 +125,20 @@ __device__ __forceinline__ T block_sum_256(T v, T* sm) {
 }
 
 // Accumulate the digits of `key` for all passes of a plan into a block-local
-// shared histogram sh[passes][RS_BINS].
+// shared histogram sh[passes][256].
 __device__ __forceinline__ void plan_hist_add(uint32_t* sh, const gt::SortPlan& p, uint64_t key) {
 #pragma unroll
   for (int q = 0; q < gt::RS_MAX_PASSES; ++q) {
     if (q < p.passes) {
       uint32_t d = uint32_t(key >> p.shift[q]) & ((1u << p.bits[q]) - 1u);
-      atomicAdd(&sh[q * gt::RS_BINS + d], 1u);
+      atomicAdd(&sh[q * 256 + d], 1u);
     }
   }
 }
 
 __device__ __forceinline__ void plan_hist_flush(const uint32_t* sh, const gt::SortPlan& p,
                                                 unsigned long long* g) {
-  for (int i = threadIdx.x; i < p.passes * gt::RS_BINS; i += blockDim.x) {
+  for (int i = threadIdx.x; i < p.passes * 256; i += blockDim.x) {
     uint32_t c = sh[i];
     if (c) atomicAdd(&g[i], (unsigned long long)c);
   }

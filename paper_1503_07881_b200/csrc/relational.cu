@@ -161,8 +161,8 @@ __global__ void __launch_bounds__(256) join_insert_kernel(const void* col, int64
                                                           gt::SortPlan plan,
                                                           unsigned long long* __restrict__ hist,
                                                           uint64_t* __restrict__ comp) {
-  __shared__ uint32_t sh[gt::RS_MAX_PASSES * gt::RS_BINS];
-  for (int i = threadIdx.x; i < plan.passes * gt::RS_BINS; i += blockDim.x) sh[i] = 0;
+  __shared__ uint32_t sh[gt::RS_MAX_PASSES * 256];
+  for (int i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const uint64_t cap = cap_mask + 1;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
