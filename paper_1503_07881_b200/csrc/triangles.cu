@@ -41,6 +41,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 namespace gtd {
 
@@ -956,7 +957,12 @@ __device__ __forceinline__ uint32_t tc_hash(int32_t x, int log_slots) {
   return (uint32_t(x) * 0x9E3779B1u) >> (32 - log_slots);
 }
 
+// Probes: kChecked = the walk pads idle lanes with TC_EMPTY and tests for it
+// before probing; an unchecked probe names an element (pad) whose lookup is
+// always false, so the walk probes every lane without the test.
 struct HashProbe {
+  static constexpr bool kChecked = true;
+  static constexpr int32_t pad = TC_EMPTY;
   int32_t* tab;
   uint32_t mask;
   int log_slots;
@@ -975,14 +981,20 @@ struct HashProbe {
   }
 };
 
-// Bit (w - v - 1) of the window (v, v + 1 + bits) for every w in N+(v). The
+// Bit w of a bitmap indexed by the element itself: the table of a task holds
+// N+(v) at ABSOLUTE window positions (w - window base, the base a multiple of
+// 32 folded into sbase), so a probe is shift, address, LDS, shift, mask with
+// no per-task subtraction, and `pad` — an element at or below v, never a
+// member, its word cleared — lets idle lanes probe without a test (ncu of the
+// C4 warp count: 13.6 instructions per element, 9 of them the probe). The
 // bitmap is addressed through its 32-bit shared-window address so every
 // probe is one LDS (a generic pointer would cost the window translation).
 struct BitmapProbe {
-  uint32_t sbase;  // shared-space address of word 0
-  int32_t base;    // v + 1
+  static constexpr bool kChecked = false;
+  uint32_t sbase;  // shared-space address of the word of element 0 (may lie below the table)
+  int32_t pad;
   __device__ __forceinline__ bool operator()(int32_t w) const {
-    const uint32_t i = uint32_t(w - base);
+    const uint32_t i = uint32_t(w);
     uint32_t x;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(sbase + ((i >> 5) << 2)) : "memory");
     return (x >> (i & 31)) & 1u;
@@ -993,6 +1005,8 @@ struct BitmapProbe {
 // top TC_SPLIT_TOP ranks in a bitmap (where R-MAT sends nearly every probe),
 // the others in a small open-addressing hash (load <= 1/4).
 struct SplitProbe {
+  static constexpr bool kChecked = true;
+  static constexpr int32_t pad = TC_EMPTY;
   uint32_t sbm;   // shared address of the bitmap words
   uint32_t stab;  // shared address of the hash slots
   int32_t top;    // n - TC_SPLIT_TOP
@@ -1084,6 +1098,12 @@ __device__ __forceinline__ uint32_t tc_wedges32(const T* __restrict__ adj, int2 
                                                 uint8_t* s_start /* [32 * TC_WIN] */) {
   const int lane = threadIdx.x & 31;
   uint32_t cnt = 0;
+  const int32_t PAD = probe.pad;  // what idle lanes hold (TC_EMPTY for the checked probes)
+  auto hit = [&](int32_t w) -> uint32_t {
+    if (std::remove_cv_t<std::remove_reference_t<Probe>>::kChecked)
+      return (w != TC_EMPTY && probe(w)) ? 1u : 0u;
+    return probe(w) ? 1u : 0u;
+  };
   // ---- long suffixes: warp per arc; the first 32*TC_UNROLL positions of the
   // NEXT arc are loaded before the current one is probed (software pipeline)
   unsigned longs = __ballot_sync(0xffffffffu, suffix.y >= TC_LONG);
@@ -1093,7 +1113,7 @@ __device__ __forceinline__ uint32_t tc_wedges32(const T* __restrict__ adj, int2 
 #pragma unroll
     for (int q = 0; q < TC_UNROLL; ++q) {
       const int k = 32 * q + lane;
-      w[q] = k < l ? int32_t(__ldg(b + k)) : TC_EMPTY;
+      w[q] = k < l ? int32_t(__ldg(b + k)) : PAD;
     }
   };
   if (longs) {
@@ -1110,8 +1130,7 @@ __device__ __forceinline__ uint32_t tc_wedges32(const T* __restrict__ adj, int2 
         fetch(j, bb, lb, wb);
       }
 #pragma unroll
-      for (int q = 0; q < TC_UNROLL; ++q)
-        if (wa[q] != TC_EMPTY) cnt += probe(wa[q]) ? 1u : 0u;
+      for (int q = 0; q < TC_UNROLL; ++q) cnt += hit(wa[q]);
       if (VEC) {  // vector walk: C4 CTA count 193 -> 180 ms; slower in the warp kernel
         // (16-bit window ranks: 357 vs 307 ms; split / hash tasks: +20 ms)
         if (la > 32 * TC_UNROLL) cnt += tc_long_tail(ba + 32 * TC_UNROLL, la - 32 * TC_UNROLL, probe);
@@ -1121,11 +1140,10 @@ __device__ __forceinline__ uint32_t tc_wedges32(const T* __restrict__ adj, int2 
 #pragma unroll
           for (int q = 0; q < TC_UNROLL; ++q) {
             const int k = k0 + 32 * q + lane;
-            w[q] = k < la ? int32_t(__ldg(ba + k)) : TC_EMPTY;
+            w[q] = k < la ? int32_t(__ldg(ba + k)) : PAD;
           }
 #pragma unroll
-          for (int q = 0; q < TC_UNROLL; ++q)
-            if (w[q] != TC_EMPTY) cnt += probe(w[q]) ? 1u : 0u;
+          for (int q = 0; q < TC_UNROLL; ++q) cnt += hit(w[q]);
         }
       }
       i = j;
@@ -1155,7 +1173,7 @@ __device__ __forceinline__ uint32_t tc_wedges32(const T* __restrict__ adj, int2 
     int32_t w[TC_WIN];
 #pragma unroll
     for (int q = 0; q < TC_WIN; ++q) {
-      w[q] = TC_EMPTY;
+      w[q] = PAD;
       if (t0 + 32 * q >= tot) continue;  // warp-uniform: nothing left
       const unsigned mine = starts[q] & (0xffffffffu >> (31 - lane));
       const int owner = mine ? int(s_start[32 * q + 31 - __clz(mine)]) : carry;
@@ -1166,8 +1184,7 @@ __device__ __forceinline__ uint32_t tc_wedges32(const T* __restrict__ adj, int2 
       if (t < tot) w[q] = int32_t(__ldg(adj + o + (t - ex)));
     }
 #pragma unroll
-    for (int q = 0; q < TC_WIN; ++q)
-      if (w[q] != TC_EMPTY) cnt += probe(w[q]) ? 1u : 0u;
+    for (int q = 0; q < TC_WIN; ++q) cnt += hit(w[q]);
     __syncwarp();
   }
   return cnt;
@@ -1238,11 +1255,14 @@ __global__ void GT_TC_LB tc_count_warp_kernel(
           else low.insert(x);
         }
       } else if (use_bm) {
-        const int nwords = int((n - 1 - v + 31) >> 5);
-        for (int i = lane; i < nwords; i += 32) bm[i] = 0u;
+        // absolute window positions w - base16 (what adj16 holds): members lie
+        // in [v + 1 - base16, n - base16), all >= 1; position 0 is the pad
+        const int w0 = (v + 1 - base16) >> 5, w1 = int((n - base16 + 31) >> 5);
+        if (lane == 0) bm[0] = 0u;
+        for (int i = w0 + lane; i < w1; i += 32) bm[i] = 0u;
         __syncwarp();
         for (int i = lane; i < dv; i += 32) {
-          const uint32_t b = uint32_t(adj_p[ov + i] - v - 1);
+          const uint32_t b = uint32_t(adj_p[ov + i] - base16);
           atomicOr(&bm[b >> 5], 1u << (b & 31));
         }
       } else {
@@ -1268,7 +1288,7 @@ __global__ void GT_TC_LB tc_count_warp_kernel(
         cnt += tc_wedges32(adj_p, sfx, probe, s_start[warp]);
       }
     } else if (use_bm) {
-      const BitmapProbe probe{uint32_t(__cvta_generic_to_shared(bm)), v + 1 - base16};
+      const BitmapProbe probe{uint32_t(__cvta_generic_to_shared(bm)), 0};
       for (int jb = task.y * TC_CHUNK; jb < end; jb += 32) {
         const int jj = jb + lane;
         const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
@@ -1306,6 +1326,8 @@ __global__ void GT_TC_LB tc_count_warp_kernel(
 constexpr int TC_CTA_SLOTS = 1 << GT_TC_CTA_LOG;
 
 struct SmemHashProbe {
+  static constexpr bool kChecked = true;
+  static constexpr int32_t pad = TC_EMPTY;
   uint32_t stab;  // shared address of the slots
   uint32_t mask;
   int log_slots;
@@ -1327,7 +1349,8 @@ __global__ void __launch_bounds__(256, GT_TC_CTA_MINB) tc_count_cta_kernel(
     const int64_t* __restrict__ off_p, const int32_t* __restrict__ adj_p,
     const int64_t* __restrict__ off_m, const int2* __restrict__ nm,
     const int2* __restrict__ tasks, int64_t n_tasks, int smem_log, int32_t* __restrict__ gtab,
-    int gtab_log, unsigned long long* __restrict__ total, int64_t n, int64_t bm_bits) {
+    int gtab_log, unsigned long long* __restrict__ total, int64_t n, int64_t bm_bits,
+    int32_t win_base) {
   extern __shared__ __align__(16) int32_t s_cta[];
   __shared__ uint8_t s_start[8][32 * TC_WIN];
   __shared__ unsigned long long s_red[8];
@@ -1364,16 +1387,22 @@ __global__ void __launch_bounds__(256, GT_TC_CTA_MINB) tc_count_cta_kernel(
     if (n - 1 - v <= bm_bits) {
       // the whole window (v, n) fits a CTA bitmap (the shared table as bits):
       // one LDS per probe instead of a hash walk (99.6% of these probes at C4)
+      // absolute positions w - win_base (win_base a multiple of 32, folded
+      // into the probe's base address); win_base itself is the pad: below
+      // every member, its word cleared
       uint32_t* bm = reinterpret_cast<uint32_t*>(s_cta);
-      const int nwords = int((n - 1 - v + 31) >> 5);
-      for (int i = threadIdx.x; i < nwords; i += 256) bm[i] = 0u;
+      const int w0 = (v + 1 - win_base) >> 5, w1 = int((n - win_base + 31) >> 5);
+      if (threadIdx.x == 0) bm[0] = 0u;
+      for (int i = w0 + threadIdx.x; i < w1; i += 256) bm[i] = 0u;
       __syncthreads();
       for (int i = threadIdx.x; i < dv; i += 256) {
-        const uint32_t b = uint32_t(adj_p[ov + i] - v - 1);
+        const uint32_t b = uint32_t(adj_p[ov + i] - win_base);
         atomicOr(&bm[b >> 5], 1u << (b & 31));
       }
       __syncthreads();
-      walk(om, begin, end, BitmapProbe{uint32_t(__cvta_generic_to_shared(bm)), v + 1});
+      walk(om, begin, end,
+           BitmapProbe{uint32_t(__cvta_generic_to_shared(bm)) - (uint32_t(win_base) >> 5) * 4u,
+                       win_base});
       continue;
     }
     const bool in_smem = 2 * int64_t(dv) <= (int64_t(1) << smem_log);
@@ -1786,6 +1815,10 @@ static int64_t count_oriented(const Oriented& o, int part, int nparts) {
   if (const char* env = getenv("GT_TC_WINDOW")) bm_bits = std::max<int64_t>(64, atoll(env));
   bm_bits = std::min<int64_t>(bm_bits, gtd::TC_BM_BITS);
   const int split_top = int(std::min<int64_t>(bm_bits / 2, gtd::TC_SPLIT_TOP));
+  // the window holds bm_cap positions; position 0 (rank n - bm_cap) is kept
+  // free as the probe pad, so bitmap tasks are the v with n - 1 - v <= bm_cap - 1
+  const int64_t bm_cap = bm_bits;
+  bm_bits = bm_cap - 1;
   // 6. work lists
   {
     Phase ph("tc.tasks", 8.0 * (n + 1) * 8);
@@ -1882,7 +1915,7 @@ static int64_t count_oriented(const Oriented& o, int part, int nparts) {
                                                           32 * tc_warps, smem));
     per_sm = std::max(per_sm, 1);
     // 16-bit copy of the window ranks for the bitmap tasks
-    const int32_t base16 = int32_t(n - bm_bits);
+    const int32_t base16 = int32_t(n - bm_cap);
     uint16_t* adj16 = reinterpret_cast<uint16_t*>(ws_get(WS_KEYS_A, size_t(m) * 2 + 64));
     if (n_bm) GT_LAUNCH(gtd::adj16_kernel, grid_cap(ceil_div64(m, 256)), 256, 0, o.adj_p, m, base16,
                         adj16);
@@ -1924,8 +1957,13 @@ static int64_t count_oriented(const Oriented& o, int part, int nparts) {
       while ((int64_t(1) << gtab_log) < 8 * max_dp) ++gtab_log;
       gtab = ws_n<int32_t>(WS_TMP4, size_t(grid) << gtab_log);
     }
+    // window base: a multiple of 32 with every rank of [win_base, n) inside
+    // the table; the threshold leaves ranks below v + 1 for the pad
+    const int64_t cta_thresh = cta_bm_bits >= 128 ? cta_bm_bits - 64 : -1;
+    const int32_t win_base =
+        cta_thresh < 0 ? 0 : int32_t(std::max<int64_t>(0, (n - cta_bm_bits + 31) & ~int64_t(31)));
     GT_LAUNCH(gtd::tc_count_cta_kernel, grid, 256, smem, o.off_p, o.adj_p, off_m, nm,
-              tasks + n_bm + n_wt, n_ct, smem_log, gtab, gtab_log, total, n, cta_bm_bits);
+              tasks + n_bm + n_wt, n_ct, smem_log, gtab, gtab_log, total, n, cta_thresh, win_base);
   }
   int64_t result = 0;
   d2h(&result, total, 8);
