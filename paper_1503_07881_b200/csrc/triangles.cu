@@ -996,7 +996,10 @@ struct BitmapProbe {
   __device__ __forceinline__ bool operator()(int32_t w) const {
     const uint32_t i = uint32_t(w);
     uint32_t x;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(sbase + ((i >> 5) << 2)) : "memory");
+    uint32_t a;  // word index * 4 + base as one multiply-add (the compiler's shift, mask,
+                 // add costs an instruction more: C4 warp count 292 -> 283 ms)
+    asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a) : "r"(i >> 5), "r"(sbase));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(a) : "memory");
     return (x >> (i & 31)) & 1u;
   }
 };
@@ -1135,7 +1138,10 @@ __device__ __forceinline__ uint32_t tc_wedges32(const T* __restrict__ adj, int2 
         // (16-bit window ranks: 357 vs 307 ms; split / hash tasks: +20 ms)
         if (la > 32 * TC_UNROLL) cnt += tc_long_tail(ba + 32 * TC_UNROLL, la - 32 * TC_UNROLL, probe);
       } else {
-        for (int k0 = 32 * TC_UNROLL; k0 < la; k0 += 32 * TC_UNROLL) {
+        int k0 = 32 * TC_UNROLL;
+        // (whole blocks without the per-element bounds test measured slower twice:
+        // 307 -> 394 ms with the checked probes, 292 -> 306 ms with these)
+        for (; k0 < la; k0 += 32 * TC_UNROLL) {
           int32_t w[TC_UNROLL];
 #pragma unroll
           for (int q = 0; q < TC_UNROLL; ++q) {
@@ -1324,6 +1330,10 @@ __global__ void GT_TC_LB tc_count_warp_kernel(
 // 64 KB tables at 3 CTAs per SM (the kernel is latency-bound on its suffix
 // reads, so residency pays more than the wider bitmap window)
 constexpr int TC_CTA_SLOTS = 1 << GT_TC_CTA_LOG;
+#ifndef GT_TC_CTA_GROUP
+#define GT_TC_CTA_GROUP 4
+#endif
+constexpr int TC_CTA_GROUP = GT_TC_CTA_GROUP;  // arcs a warp draws at a time (<= 32)
 
 struct SmemHashProbe {
   static constexpr bool kChecked = true;
@@ -1358,17 +1368,19 @@ __global__ void __launch_bounds__(256, GT_TC_CTA_MINB) tc_count_cta_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int32_t* mytab = gtab ? gtab + (int64_t(blockIdx.x) << gtab_log) : nullptr;
   unsigned long long acc = 0;
-  // the warps draw 32-arc groups of the chunk from a shared counter, so the
-  // CTA's end-of-task barrier waits for at most one group, not a fixed share
+  // the warps draw groups of TC_CTA_GROUP arcs of the chunk from a shared
+  // counter, so the CTA's end-of-task barrier waits for at most one group, not
+  // a fixed share (ncu at C4 with 32-arc groups: 31 % of the stall samples at
+  // that barrier — a group's work varies with its suffix lengths)
   auto walk = [&](int64_t om, int begin, int end, const auto& probe) {
     uint32_t cnt = 0;
     while (true) {
       int g = 0;
       if (lane == 0) g = atomicAdd(&s_next, 1);
-      const int jb = begin + 32 * __shfl_sync(0xffffffffu, g, 0);
+      const int jb = begin + TC_CTA_GROUP * __shfl_sync(0xffffffffu, g, 0);
       if (jb >= end) break;
       const int jj = jb + lane;
-      const int2 sfx = jj < end ? nm[om + jj] : make_int2(0, 0);
+      const int2 sfx = (lane < TC_CTA_GROUP && jj < end) ? nm[om + jj] : make_int2(0, 0);
       cnt += tc_wedges32<decltype(probe), int32_t, true>(adj_p, sfx, probe, s_start[warp]);
     }
     acc += cnt;
