@@ -1052,9 +1052,18 @@ __device__ __forceinline__ int tc_log_slots(int64_t d, int cap_log) {
 // of a suffix shorter than 32*TC_UNROLL idles lanes, the flattened walk pays
 // the owner lookup. The three constants were swept on C2
 // (scripts/sweep_tc_consts.sh): 16/4/8 -> 64/7/4 took the count 11.3 -> 8.8 ms.
-constexpr int TC_WIN = 7;
-constexpr int TC_LONG = 64;
-constexpr int TC_UNROLL = 4;
+#ifndef GT_TC_WIN
+#define GT_TC_WIN 7
+#endif
+#ifndef GT_TC_LONG
+#define GT_TC_LONG 64
+#endif
+#ifndef GT_TC_UNROLL
+#define GT_TC_UNROLL 4
+#endif
+constexpr int TC_WIN = GT_TC_WIN;
+constexpr int TC_LONG = GT_TC_LONG;
+constexpr int TC_UNROLL = GT_TC_UNROLL;
 
 // The part of a long suffix past its first 32*TC_UNROLL elements, walked by
 // the warp with 16-byte vector loads (4 ranks per load): at C4 most probes

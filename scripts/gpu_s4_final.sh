@@ -4,7 +4,6 @@
 cd "$GRAFT_REPO_ROOT"
 mkdir -p gpurun_out
 T=${1:-s4f}
-timeout 600 python scripts/probe_lanes.py c4 > gpurun_out/${T}_lanes.log 2>&1
 timeout 2700 python -m pytest tests -x -q -m gpu --durations=15 > gpurun_out/${T}_pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/${T}_pytest_gpu.log
 cp gpurun_out/reference_suite_on_dropin.log gpurun_out/${T}_reference_suite.log 2>/dev/null
