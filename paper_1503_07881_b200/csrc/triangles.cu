@@ -186,67 +186,77 @@ __global__ void __launch_bounds__(256) cand_degree_kernel(
     }
   }
   __syncthreads();
-  // row start (tile-relative slot) and out-row extent of relative row ri
-  auto c_at = [&](int ri) -> int64_t { return staged ? s_c[ri] : cat[r0 + ri] - e0; };
-  auto o_at = [&](int ri) -> int64_t { return staged ? s_o[ri] : out_off[r0 + ri] - oo0; };
-
-  // ---- neighbour ids of the tile (all loads issued before any is consumed) ----
-  int32_t j[PER];
+  // The rest of the tile, generic over the index type: 32-bit tile-relative
+  // offsets when the rows are staged (every tile but those of isolated-node
+  // runs; ncu: the kernel is issue-bound and most of its integer work was
+  // 64-bit offset arithmetic), 64-bit offsets read from global memory otherwise.
+  // c_at(ri): row start (tile-relative slot); o_at(ri): out-row extent.
+  auto tile_body = [&](auto zero, auto c_at, auto o_at) {
+    using I = decltype(zero);
+    // ---- neighbour ids of the tile (all loads issued before any is consumed) ----
+    int32_t j[PER];
 #pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    const int t = q * 256 + tid;
-    j[q] = 0;
-    if (t < tn) {
-      const int ri = s_row[t];
-      const int64_t c = c_at(ri), oa = o_at(ri), no = o_at(ri + 1) - oa;
-      const int64_t k = t - c;
-      j[q] = k < no ? out_adj[oo0 + oa + k] : in_adj[(e0 + c) - (oo0 + oa) + (k - no)];
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < PER; ++q) s_j[q * 256 + tid] = j[q];
-  __syncthreads();
-
-  // drop self-loops and in-slots whose source is also an out-neighbour
-#pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    const int t = q * 256 + tid;
-    const bool valid = t < tn;
-    bool cand = false;
-    int ri = -1;
-    if (valid) {
-      ri = s_row[t];
-      cand = int64_t(j[q]) != r0 + ri;
-      const int64_t c = c_at(ri), oa = o_at(ri), no = o_at(ri + 1) - oa;
-      if (cand && t - c >= no) {
-        if (c >= 0) {  // the whole out-row [c, c+no) precedes t inside the tile
-          int lo = int(c), hi = int(c + no);
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (s_j[mid] < j[q]) lo = mid + 1;
-            else hi = mid;
-          }
-          cand = !(lo < int(c + no) && s_j[lo] == j[q]);
-        } else {
-          cand = !bsearch_in(out_adj + oo0 + oa, no, j[q]);
-        }
+    for (int q = 0; q < PER; ++q) {
+      const int t = q * 256 + tid;
+      j[q] = 0;
+      if (t < tn) {
+        const int ri = s_row[t];
+        const I c = c_at(ri), oa = o_at(ri), no = o_at(ri + 1) - oa;
+        const I k = I(t) - c;
+        j[q] = k < no ? out_adj[oo0 + oa + k] : in_adj[(e0 - oo0) + (c - oa) + (k - no)];
       }
     }
-    // per-row counts: the 32 slots of a warp step are consecutive, so each
-    // row is a run of lanes; the first lane of a run adds the run's count
-    const unsigned active = __ballot_sync(0xffffffffu, valid);
-    const unsigned kb = __ballot_sync(0xffffffffu, cand);
-    if (lane == 0 && active) keep_bits[(e0 + q * 256 + warp * 32) >> 5] = kb;
-    const int prev = __shfl_up_sync(0xffffffffu, ri, 1);
-    const bool head = valid && (lane == 0 || prev != ri);
-    const unsigned heads = __ballot_sync(0xffffffffu, head);
-    if (head) {
-      const unsigned after = heads & ~((2u << lane) - 1u);  // later heads
-      const unsigned runm = (after ? (after & (0u - after)) - 1u : 0xffffffffu) & ~((1u << lane) - 1u);
-      const int cnt = __popc(kb & runm);
-      if (cnt) atomicAdd(&deg[r0 + ri], cnt);
+#pragma unroll
+    for (int q = 0; q < PER; ++q) s_j[q * 256 + tid] = j[q];
+    __syncthreads();
+
+    // drop self-loops and in-slots whose source is also an out-neighbour
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int t = q * 256 + tid;
+      const bool valid = t < tn;
+      bool cand = false;
+      int ri = -1;
+      if (valid) {
+        ri = s_row[t];
+        cand = int64_t(j[q]) != r0 + ri;
+        const I c = c_at(ri), oa = o_at(ri), no = o_at(ri + 1) - oa;
+        if (cand && I(t) - c >= no) {
+          if (c >= 0) {  // the whole out-row [c, c+no) precedes t inside the tile
+            int lo = int(c), hi = int(c + no);
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (s_j[mid] < j[q]) lo = mid + 1;
+              else hi = mid;
+            }
+            cand = !(lo < int(c + no) && s_j[lo] == j[q]);
+          } else {
+            cand = !bsearch_in(out_adj + oo0 + oa, no, j[q]);
+          }
+        }
+      }
+      // per-row counts: the 32 slots of a warp step are consecutive, so each
+      // row is a run of lanes; the first lane of a run adds the run's count
+      const unsigned active = __ballot_sync(0xffffffffu, valid);
+      const unsigned kb = __ballot_sync(0xffffffffu, cand);
+      if (lane == 0 && active) keep_bits[(e0 + q * 256 + warp * 32) >> 5] = kb;
+      const int prev = __shfl_up_sync(0xffffffffu, ri, 1);
+      const bool head = valid && (lane == 0 || prev != ri);
+      const unsigned heads = __ballot_sync(0xffffffffu, head);
+      if (head) {
+        const unsigned after = heads & ~((2u << lane) - 1u);  // later heads
+        const unsigned runm = (after ? (after & (0u - after)) - 1u : 0xffffffffu) & ~((1u << lane) - 1u);
+        const int cnt = __popc(kb & runm);
+        if (cnt) atomicAdd(&deg[r0 + ri], cnt);
+      }
     }
-  }
+  };
+  if (staged)
+    tile_body(int32_t(0), [&](int ri) -> int32_t { return s_c[ri]; },
+              [&](int ri) -> int32_t { return s_o[ri]; });
+  else
+    tile_body(int64_t(0), [&](int ri) -> int64_t { return cat[r0 + ri] - e0; },
+              [&](int ri) -> int64_t { return out_off[r0 + ri] - oo0; });
 }
 
 // ---- rank (algorithms.py:103-106: lexsort by (degree, id)) ------------------
